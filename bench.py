@@ -1,0 +1,336 @@
+"""bench.py — LOPC hot path on B200: compress + decompress throughput.
+
+One step = one pass of the whole hot path over one
+synthetic field: lopc_compress (quantize -> repair to the fixpoint -> chunked
+encode with look-back placement) followed by lopc_decompress, input resident
+in HBM.  value = raw input GB (all ranks) / (max over ranks of the summed
+device time of the K timed steps), in GB/s.  L2 (126 MB) is flushed between
+steps by writing a 512 MB buffer outside the timed events.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg2]
+  python bench.py --impl reference ...   # the CPU oracle arm (rank 0 only)
+
+Multi-GPU (torchrun): every rank compresses its own field of the chosen
+config (weak scaling, no data-path collective: the slab mode with halo
+exchange is not built yet); the barrier + max-over-ranks
+timing of the contract is kept.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+from synth.fields import CONFIGS, eps_noa, sha256  # noqa: E402
+
+METRIC = "compress/decompress GB/s at 1/2/4/8 B200 (%HBM roofline); ratio; 0 order violations"
+WORKLOAD = {
+    "cfg1": "cfg1: 2D f32 64x64 sum-of-Gaussians with plateaus/ties, NOA 1e-2",
+    "cfg2": "cfg2: 3D f32 100x500x500 Isabel-shaped synthetic field, NOA 1e-3",
+    "cfg3": "cfg3: 3D f32 512^3 NYX-shaped log-normal density, NOA 1e-4",
+    "cfg4": "cfg4: 2D f32 1800x3600 CESM-ATM-shaped field with near-ties, NOA 1e-3",
+}
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy read+write)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self.proc = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 7:
+                self.samples.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[3 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def oracle_sample(cfg_name: str, x: np.ndarray, eps: float, budget_s: float):
+    """The CPU oracle (single thread) on a bounded crop of the same field:
+    leading z-planes (3D) or rows (2D), compress + decompress, repeated until
+    ~budget_s.  Returns (GB/s, description)."""
+    import oracle
+
+    oracle.build()
+    planes = max(1, x.shape[0] // 12) if x.ndim == 3 else max(1, x.shape[0] // 8)
+    crop = np.ascontiguousarray(x[:planes])
+    t0 = time.perf_counter()
+    done = 0
+    reps = 0
+    while True:
+        st = oracle.compress(crop, eps)
+        oracle.decompress(st)
+        done += crop.nbytes
+        reps += 1
+        if time.perf_counter() - t0 > budget_s:
+            break
+    dt = time.perf_counter() - t0
+    desc = (f"oracle compress+decompress of the leading {planes} of {x.shape[0]} "
+            f"{'z-planes' if x.ndim == 3 else 'rows'} of {cfg_name} ({crop.nbytes / 1e6:.1f} MB) x{reps}, "
+            f"{dt:.1f} s, 1 thread on {cpu_model()}")
+    return done / dt / 1e9, desc
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    cfg = CONFIGS[args.config]
+    x = cfg.generate()
+    eps = eps_noa(x, cfg.rel)
+    times = []
+    desc = ""
+    per = max(2.0, 60.0 / max(1, args.steps + args.warmup))
+    for i in range(args.warmup + args.steps):
+        v, desc = oracle_sample(args.config, x, eps, per)
+        if i >= args.warmup:
+            times.append(v)
+    value = statistics.median(times)
+    line = {"metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic", "impl": "reference",
+            "config": {"workload": WORKLOAD[args.config], "sample": "bounded crop, see cpu_baseline"},
+            "cpu_baseline": {"value": value, "unit": "GB/s", "cores": 1, "kind": "oracle", "sample": desc},
+            "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="cfg2", choices=sorted(WORKLOAD))
+    ap.add_argument("--impl", default="lopc", choices=["lopc", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=15.0)
+    args = ap.parse_args()
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+
+    import torch
+
+    import paper_2603_26968_b200 as lopc
+
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    lopc.load()
+    cfg = CONFIGS[args.config]
+    x_np = cfg.generate()
+    eps = eps_noa(x_np, cfg.rel)
+    x = torch.from_numpy(x_np).cuda()
+    raw = x_np.nbytes
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
+    st_buf = torch.empty(lopc.compress_bound(x.shape, x.dtype), dtype=torch.uint8, device="cuda")
+    y = torch.empty_like(x)
+
+    def step():
+        st = lopc.compress(x, eps, out=st_buf)
+        lopc.decompress(st, out=y)
+        return st
+
+    for _ in range(args.warmup):
+        st = step()
+    torch.cuda.synchronize()
+    # correctness of the benchmarked configuration: order / bound / stability
+    import oracle  # test infrastructure, outside the timed region
+
+    y_np = y.cpu().numpy()
+    violations = oracle.order_violations(x_np, y_np) if rank == 0 else 0
+    bound_bad = oracle.bound_violations(x_np, y_np, eps) if rank == 0 else 0
+    nbytes_stream = int(st.numel())
+
+    lopc.set_timing(True)
+    comp_ms, dec_ms, kern = [], [], {"quant_repair": [], "sweep": [], "encode": [], "decode": []}
+    passes, tiles = [], []
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            flush.fill_(1)
+            ev[0].record()
+            st = lopc.compress(x, eps, out=st_buf)
+            ev[1].record()
+            sc = lopc.last_stats()
+            lopc.decompress(st, out=y)
+            ev[2].record()
+            sd = lopc.last_stats()
+            torch.cuda.synchronize()
+            comp_ms.append(ev[0].elapsed_time(ev[1]))
+            dec_ms.append(ev[1].elapsed_time(ev[2]))
+            kern["quant_repair"].append(sc["ms_quant_repair"])
+            kern["sweep"].append(sc["ms_sweep"])
+            kern["encode"].append(sc["ms_encode"])
+            kern["decode"].append(sd["ms_decode"])
+            passes.append(sc["sweep_passes"])
+            tiles.append(sc["tiles_processed"])
+    torch.cuda.synchronize()
+    lopc.set_timing(False)
+    total_ms = sum(comp_ms) + sum(dec_ms)
+    if dist:
+        t = torch.tensor([total_ms, sum(comp_ms), sum(dec_ms)], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms, cm, dm = (float(v) for v in t.tolist())
+    else:
+        cm, dm = sum(comp_ms), sum(dec_ms)
+    K = args.steps
+    value = raw * world * K / (total_ms / 1e3) / 1e9
+
+    # ---- e2e through the C-ABI with HOST (pinned) buffers -------------------
+    xh = torch.from_numpy(x_np).pin_memory()
+    sth = torch.empty(st_buf.numel(), dtype=torch.uint8).pin_memory()
+    yh = torch.empty(x_np.shape, dtype=torch.float32 if x_np.dtype == np.float32 else torch.float64).pin_memory()
+    for _ in range(2):
+        s2 = lopc.compress(xh, eps, out=sth)
+        lopc.decompress(s2, out=yh)
+    e2e_ms = []
+    for _ in range(max(3, K // 2)):
+        flush.fill_(1)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        s2 = lopc.compress(xh, eps, out=sth)
+        lopc.decompress(s2, out=yh)
+        e2e_ms.append((time.perf_counter() - t0) * 1e3)
+    e2e_step = statistics.median(e2e_ms)
+    if dist:
+        t = torch.tensor([e2e_step], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_step = float(t.item())
+    e2e_val = raw * world / (e2e_step / 1e3) / 1e9
+
+    if rank != 0:
+        if dist:
+            dist.destroy_process_group()
+        return
+
+    # ---- roofline of the dominant kernel ----------------------------------
+    peak, peak_src = load_peaks()
+    n = x_np.size
+    k = x_np.itemsize
+    F = 2 if x_np.ndim == 3 else 1
+    med = {kk: statistics.median(v) for kk, v in kern.items()}
+    tiles_pts = 2048
+    alg = {
+        # read x, write flags + s
+        "quant_repair": n * (k + F + 4),
+        # per processed tile point: read flags + s (write traffic not counted)
+        "sweep": statistics.median(tiles) * tiles_pts * (F + 4),
+        # read x + s, write the stream
+        "encode": n * (k + 4) + nbytes_stream,
+        # read the stream, write x^
+        "decode": nbytes_stream + n * k,
+    }
+    dom = max(med, key=lambda kk: med[kk])
+    achieved = alg[dom] / (med[dom] / 1e3) / 1e9 if med[dom] > 0 else 0.0
+    per_kernel = {kk: {"ms": med[kk], "alg_bytes": alg[kk],
+                       "GBps": (alg[kk] / (med[kk] / 1e3) / 1e9) if med[kk] > 0 else None} for kk in med}
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", f"traffic_{args.config}.json")
+    if os.path.exists(tp):
+        traffic = json.load(open(tp)).get(f"k_{dom}")
+
+    cpu = None
+    if not args.no_cpu_baseline:
+        v, desc = oracle_sample(args.config, x_np, eps, args.cpu_budget)
+        cpu = {"value": v, "unit": "GB/s", "cores": 1, "kind": "oracle", "sample": desc}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": K, "warmup": args.warmup,
+        "ms_per_step": total_ms / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f32" if k == 4 else "f64", "data": "synthetic",
+        "config": {"workload": WORKLOAD[args.config], "dims": list(x_np.shape), "eps": eps,
+                   "input_sha256": sha256(x_np), "l2": "flushed (512 MB write) between steps",
+                   "parallelism": f"replicas x{world}" if world > 1 else "single GPU"},
+        "compress_GBps": raw * world * K / (cm / 1e3) / 1e9,
+        "decompress_GBps": raw * world * K / (dm / 1e3) / 1e9,
+        "ratio": raw / nbytes_stream, "stream_bytes": nbytes_stream,
+        "order_violations": violations, "bound_violations": bound_bad,
+        "sweep_passes": statistics.median(passes), "tiles_processed": statistics.median(tiles),
+        "per_kernel": per_kernel,
+        "roofline": {"kernel": f"k_{dom}", "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src},
+        "cpu_baseline": cpu,
+        "e2e": {"value": e2e_val, "unit": "GB/s", "h2d_bytes_per_step": raw + nbytes_stream,
+                "d2h_bytes_per_step": nbytes_stream + raw,
+                "note": "lopc_compress/lopc_decompress on pinned host buffers, staging copies inside the call"},
+        "gpu_launches": 4 * K,
+        "clocks": clk.summary(),
+    }
+    print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

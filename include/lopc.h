@@ -1,0 +1,134 @@
+/* lopc.h — C-ABI of liblopc.so, the B200 (sm_100a) LOPC hot path.
+ *
+ * LOPC (arxiv 2603.26968, PAPER.md): error-bounded quantization (§IV.A,
+ * P:109-116), local-order repair of subbins to a fixpoint (§IV.B, Alg. 1
+ * P:127-154, Alg. 2), chunked lossless coding (§IV.C)
+ * and the matching decoder.  Readings of silent passages and
+ * the stream format are in DESIGN.md §3-§4.
+ *
+ * Conventions for every entry point:
+ *  - Grid: dims[0..ndims-1] slowest -> fastest, ndims in {2,3}; values are
+ *    row-major with the last dim contiguous (G3).  Each dim and the product
+ *    N must be <= 2^40.  N = 0 is allowed (header-only stream).
+ *  - dtype: LOPC_F32 or LOPC_F64.
+ *  - Buffers are owned by the caller.  The library never frees or retains a
+ *    caller pointer after return.  `in`/`out` may be device pointers or host
+ *    pointers (pinned or pageable); host buffers are staged through the
+ *    workspace with cudaMemcpyAsync inside the call.  All other pointers
+ *    (workspace) are device pointers.
+ *  - The *_ex calls take an explicit workspace (device memory, >= the size the
+ *    matching *_workspace_bytes function returns, 256-byte aligned) and a
+ *    cudaStream_t (passed as void*; NULL = legacy default stream).  The plain
+ *    calls use a grow-only internal workspace on the current device and the
+ *    legacy default stream.  No allocation happens inside *_ex.
+ *  - Every call blocks until its result code is known (one device->host read
+ *    of an 8..256-byte status block at the end).
+ *  - Return value: LOPC_OK (0) or a negative LOPC_E_* code.  On LOPC_E_NOSPACE
+ *    from a compress call, *out_bytes holds the size required.  Output buffer
+ *    contents are unspecified on error.
+ *  - Determinism: the same (x, dims, dtype, eps) gives the same bytes for any
+ *    launch configuration, stream or GPU (the repair result is the unique least
+ *    fixpoint; chunk payloads are placed by a prefix sum).
+ *  - NaN, +-Inf and values whose bin exceeds BINMAX (2^31-2 for f32, 2^50 for
+ *    f64) are not errors: they are stored losslessly (escapes, G8-G11).
+ */
+#ifndef LOPC_H
+#define LOPC_H
+#include <stddef.h>
+#include <stdint.h>
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LOPC_ABI_VERSION 1
+
+typedef enum { LOPC_F32 = 0, LOPC_F64 = 1 } lopc_dtype;
+
+enum {
+  LOPC_OK = 0,
+  LOPC_E_ARG = -1,      /* null pointer, bad dtype, eps not finite / not in [2^-900, 2^1000] */
+  LOPC_E_SHAPE = -2,    /* ndims not 2/3, a dim or N > 2^40 */
+  LOPC_E_NOSPACE = -3,  /* output or workspace too small */
+  LOPC_E_CORRUPT = -4,  /* malformed stream (header, size table or payload) */
+  LOPC_E_VERSION = -5,  /* stream version != 1 */
+  LOPC_E_CUDA = -6,     /* CUDA runtime error (message: lopc_last_error_string) */
+  LOPC_E_NCCL = -7,     /* reserved for the multi-GPU slab mode */
+  LOPC_E_INTERNAL = -8  /* a self-check failed (bound re-check a4, subbin overflow, pass cap) */
+};
+
+/* Worst-case stream size: 64 + 8C + 2 * 16384 * C bytes, C = ceil(N / (16384/k)). */
+size_t lopc_compress_bound(int ndims, const uint64_t* dims, int dtype);
+
+/* Workspace bytes for lopc_compress_ex.  host_io != 0 adds room to stage a
+ * host input (N*k) and a host output (lopc_compress_bound). */
+size_t lopc_compress_workspace_bytes(int ndims, const uint64_t* dims, int dtype, int host_io);
+
+/* Workspace bytes for lopc_decompress_ex of a stream of in_bytes bytes that
+ * decodes to out_bytes bytes; host_io != 0 adds staging for both. */
+size_t lopc_decompress_workspace_bytes(size_t in_bytes, size_t out_bytes, int host_io);
+
+/* Compress x (N values of dtype) with absolute error bound eps (ABS; for NOA
+ * the caller passes eps = rel * (max - min)).  *out_bytes: in = the
+ * capacity of out, out = bytes written (or required, on LOPC_E_NOSPACE). */
+int lopc_compress(const void* in, int ndims, const uint64_t* dims, int dtype, double eps, void* out,
+                  size_t* out_bytes);
+int lopc_compress_ex(const void* in, int ndims, const uint64_t* dims, int dtype, double eps, void* out,
+                     size_t* out_bytes, void* workspace, size_t workspace_bytes, void* stream);
+
+/* Decompress a stream of in_bytes bytes into out (capacity out_capacity
+ * bytes, must hold N*k).  The header is validated on the device; corrupt
+ * streams return LOPC_E_CORRUPT without partial-output guarantees. */
+int lopc_decompress(const void* in, size_t in_bytes, void* out, size_t out_capacity);
+int lopc_decompress_ex(const void* in, size_t in_bytes, void* out, size_t out_capacity, void* workspace,
+                       size_t workspace_bytes, void* stream);
+
+/* Host-side parse of a stream header (host pointer, >= 64 bytes).  dims3 gets
+ * (d0, d1, d2) with d0 = 1 for 2D.  Any output pointer may be NULL. */
+int lopc_stream_info(const void* host_hdr, size_t n, int* ndims, uint64_t* dims3, int* dtype, double* eps,
+                     uint64_t* n_elems, uint32_t* n_chunks);
+
+/* Parity/diagnostic hook: run steps a1-a3 only and copy the flags (as u16,
+ * Alg. 1 loop 2, slot order G2) and the final subbins (u32) into the given
+ * device buffers (N entries each; either may be NULL).  Uses the
+ * lopc_compress_ex workspace. */
+int lopc_repair_ex(const void* in, int ndims, const uint64_t* dims, int dtype, double eps, uint16_t* flags_out,
+                   uint32_t* subbins_out, void* workspace, size_t workspace_bytes, void* stream);
+
+/* Statistics of the last compress/decompress call on this process. */
+typedef struct {
+  uint64_t n_elems;
+  uint64_t n_chunks;
+  uint64_t n_tiles;
+  uint64_t sweep_passes;      /* global passes of k_sweep after k_quant_repair */
+  uint64_t tiles_processed;   /* sum of active tiles over those passes */
+  uint64_t inner_iters;       /* sum of tile-local relaxation iterations */
+  uint64_t escapes;
+  uint64_t bin_bytes;
+  uint64_t sub_bytes;
+  uint64_t total_bytes;
+  uint32_t max_subbin;
+  uint32_t timing_valid;      /* 1 if the ms_* fields were measured (lopc_set_timing) */
+  float ms_h2d;               /* host->device staging */
+  float ms_quant_repair;      /* k_quant_repair */
+  float ms_sweep;             /* k_sweep */
+  float ms_encode;            /* k_encode */
+  float ms_decode;            /* k_decode */
+  float ms_d2h;               /* device->host staging */
+  float ms_total;             /* whole call on the stream */
+} lopc_stats;
+
+int lopc_last_stats(lopc_stats* out);
+
+/* Enable (1) / disable (0) per-kernel CUDA-event timing in lopc_stats. */
+void lopc_set_timing(int enable);
+
+/* Message for a return code; lopc_last_error_string() adds CUDA detail. */
+const char* lopc_strerror(int code);
+const char* lopc_last_error_string(void);
+
+int lopc_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -73,6 +73,8 @@ def lib():
         L.lopc_ref_order_violations.restype = C.c_uint64
         L.lopc_ref_bound_violations.argtypes = [P, P, C.c_uint64, I, D]
         L.lopc_ref_bound_violations.restype = C.c_uint64
+        L.lopc_ref_encode_chunk.argtypes = [P, C.c_uint64, I, D, P, C.c_uint64, P, P]
+        L.lopc_ref_encode_chunk.restype = I
         L.lopc_ref_certify.argtypes = [P, I, U64P, I, D, P]
         L.lopc_ref_certify.restype = C.c_uint64
         _lib = L
@@ -259,6 +261,15 @@ def bound_violations(x: np.ndarray, y: np.ndarray, eps: float) -> int:
     x = np.ascontiguousarray(x)
     y = np.ascontiguousarray(y, dtype=x.dtype)
     return int(lib().lopc_ref_bound_violations(_ptr(x), _ptr(y), x.size, _dt(x), eps))
+
+
+def encode_chunk(x: np.ndarray, eps: float, s: np.ndarray, c: int):
+    x = np.ascontiguousarray(x)
+    s = np.ascontiguousarray(s, dtype=np.uint32)
+    out = np.empty(2 * 16384, np.uint8)
+    sz = (C.c_uint32 * 2)()
+    _chk(lib().lopc_ref_encode_chunk(_ptr(x), x.size, _dt(x), eps, _ptr(s), c, _ptr(out), sz), "encode_chunk")
+    return out[: sz[0]].tobytes(), out[sz[0]: sz[0] + sz[1]].tobytes()
 
 
 def certify(x: np.ndarray, eps: float, s: np.ndarray) -> int:

@@ -816,6 +816,48 @@ out:
   return rc;
 }
 
+/* One chunk's two payloads from x and a subbin field s (used to check a GPU
+ * stream chunk by chunk after the Bellman certificate has shown that s is
+ * the fixpoint).  out receives bin payload then subbin
+ * payload; sizes2 = {bin_size, sub_size}. */
+int lopc_ref_encode_chunk(const void* x, uint64_t n, int dtype, double eps, const uint32_t* s, uint64_t c,
+                          void* out, uint32_t* sizes2) {
+  if ((dtype != 0 && dtype != 1) || check_eps(eps)) return E_ARG;
+  int k = dtype == 0 ? 4 : 8;
+  uint64_t W = CHUNK_BYTES / (uint64_t)k;
+  if (c * W >= n) return E_ARG;
+  uint8_t *bw = (uint8_t*)calloc(CHUNK_BYTES, 1), *sw = (uint8_t*)calloc(CHUNK_BYTES, 1);
+  uint8_t *t1 = (uint8_t*)malloc(CHUNK_BYTES), *t2 = (uint8_t*)malloc(2 * CHUNK_BYTES),
+          *t3 = (uint8_t*)malloc(2 * CHUNK_BYTES);
+  int rc = 0;
+  if (!bw || !sw || !t1 || !t2 || !t3) {
+    rc = E_INTERNAL;
+    goto out;
+  }
+  for (uint64_t i = c * W; i < n && i < (c + 1) * W; i++) {
+    int64_t b;
+    uint64_t bwv, swv;
+    if (lopc_ref_bin(value_at(x, i, dtype), eps, dtype, &b)) {
+      bwv = (uint64_t)b & mask_k(k);
+      swv = s[i];
+    } else {
+      bwv = dtype == 0 ? 0x80000000ull : 0x8000000000000000ull;
+      swv = bits_at(x, i, dtype);
+    }
+    word_put(bw + (i - c * W) * k, k, bwv);
+    word_put(sw + (i - c * W) * k, k, swv);
+  }
+  sizes2[0] = (uint32_t)encode_bin_chunk(bw, k, (uint8_t*)out, t1, t2, t3);
+  sizes2[1] = (uint32_t)encode_sub_chunk(sw, k, (uint8_t*)out + sizes2[0], t1, t2, t3);
+out:
+  free(bw);
+  free(sw);
+  free(t1);
+  free(t2);
+  free(t3);
+  return rc;
+}
+
 int lopc_ref_stream_info(const void* in, size_t nbytes, int* ndims, uint64_t* dims3, int* dtype,
                          double* eps, uint64_t* n_elems, uint32_t* n_chunks_out) {
   const uint8_t* p = (const uint8_t*)in;

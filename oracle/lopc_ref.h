@@ -69,6 +69,11 @@ int lopc_ref_stream_info(const void* in, size_t n, int* ndims, uint64_t* dims3, 
 /* per-chunk sizes (u32 pairs) of a stream: copies 2*C u32 into sizes. */
 int lopc_ref_chunk_sizes(const void* in, size_t n, uint32_t* sizes, uint32_t cap_pairs);
 
+/* one chunk (elements [c*W, min((c+1)W, n))) from x and a given subbin
+ * field s: out (>= 32768 B) gets bin payload then subbin payload. */
+int lopc_ref_encode_chunk(const void* x, uint64_t n, int dtype, double eps, const uint32_t* s, uint64_t c,
+                          void* out, uint32_t* sizes2);
+
 /* --- Lossless stages (G17-G21) ---------------------- */
 void lopc_ref_diffnb(const void* words, size_t W, int k, void* out);
 void lopc_ref_undiffnb(const void* in, size_t W, int k, void* words);

@@ -1,0 +1,615 @@
+// lopc_api.cu — host orchestration behind include/lopc.h (liblopc.so).
+//
+// compress:   [H2D stage] -> k_quant_repair -> k_sweep (cooperative, device-
+//             side termination) -> k_encode (look-back placement, header) ->
+//             one D2H read of the status block -> [D2H stage]
+// decompress: [H2D stage] -> k_decode (persistent, header validated on the
+//             device) -> one D2H read of the status block -> [D2H stage]
+//
+// Scratch comes only from the caller's workspace; nothing is allocated inside
+// the *_ex calls.  See DESIGN.md §7 for the HBM layout.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+
+#include "../../include/lopc.h"
+#include "lopc_codec.cuh"
+#include "lopc_repair.cuh"
+
+using namespace lopc;
+
+namespace {
+
+char g_errmsg[512] = "";
+lopc_stats g_stats{};
+int g_timing = 0;
+
+int set_cuda_error(cudaError_t e, const char* where) {
+  snprintf(g_errmsg, sizeof(g_errmsg), "%s: %s (%s)", where, cudaGetErrorName(e), cudaGetErrorString(e));
+  return LOPC_E_CUDA;
+}
+
+#define CK(call)                                      \
+  do {                                                \
+    cudaError_t e_ = (call);                          \
+    if (e_ != cudaSuccess) return set_cuda_error(e_, #call); \
+  } while (0)
+
+struct Shape {
+  int ndims, dtype, k;
+  uint64_t d0, d1, d2, n, C;
+};
+
+int make_shape(int ndims, const uint64_t* dims, int dtype, Shape& s) {
+  if (dtype != LOPC_F32 && dtype != LOPC_F64) return LOPC_E_ARG;
+  if (!dims) return LOPC_E_ARG;
+  if (ndims != 2 && ndims != 3) return LOPC_E_SHAPE;
+  const uint64_t lim = 1ull << 40;
+  s.ndims = ndims;
+  s.dtype = dtype;
+  s.k = dtype == LOPC_F32 ? 4 : 8;
+  if (ndims == 2) {
+    s.d0 = 1;
+    s.d1 = dims[0];
+    s.d2 = dims[1];
+  } else {
+    s.d0 = dims[0];
+    s.d1 = dims[1];
+    s.d2 = dims[2];
+  }
+  if (s.d0 > lim || s.d1 > lim || s.d2 > lim) return LOPC_E_SHAPE;
+  if (s.d0 && s.d1 && (s.d0 * s.d1 > lim || s.d0 * s.d1 * s.d2 > lim)) return LOPC_E_SHAPE;
+  s.n = s.d0 * s.d1 * s.d2;
+  const uint64_t W = kChunkBytes / s.k;
+  s.C = (s.n + W - 1) / W;
+  return LOPC_OK;
+}
+
+int check_eps(double eps) {
+  if (!(eps >= std::ldexp(1.0, -900) && eps <= std::ldexp(1.0, 1000))) return LOPC_E_ARG;
+  return LOPC_OK;
+}
+
+inline size_t al(size_t v) { return (v + 255) & ~size_t(255); }
+
+struct CLayout {
+  size_t ctr, stamp, state, zero_end, lists, flags, s, stage_in, stage_out, total;
+  int ntz, nty, ntx;
+  uint64_t ntiles;
+};
+
+CLayout compress_layout(const Shape& s, bool host_in, bool host_out) {
+  CLayout L{};
+  if (s.ndims == 3) {
+    L.ntz = (int)((s.d0 + Geo<3>::TZ - 1) / Geo<3>::TZ);
+    L.nty = (int)((s.d1 + Geo<3>::TY - 1) / Geo<3>::TY);
+    L.ntx = (int)((s.d2 + Geo<3>::TX - 1) / Geo<3>::TX);
+  } else {
+    L.ntz = 1;
+    L.nty = (int)((s.d1 + Geo<2>::TY - 1) / Geo<2>::TY);
+    L.ntx = (int)((s.d2 + Geo<2>::TX - 1) / Geo<2>::TX);
+  }
+  L.ntiles = s.n ? (uint64_t)L.ntz * L.nty * L.ntx : 0;
+  size_t o = 0;
+  L.ctr = o;
+  o += al(sizeof(Counters));
+  L.stamp = o;
+  o += al(4 * L.ntiles);
+  L.state = o;
+  o += al(8 * s.C);
+  L.zero_end = o;
+  L.lists = o;
+  o += al(3 * 4 * L.ntiles);
+  L.flags = o;
+  o += al((s.ndims == 3 ? 2 : 1) * s.n);
+  L.s = o;
+  o += al(4 * s.n);
+  L.stage_in = o;
+  if (host_in) o += al(s.k * s.n);
+  L.stage_out = o;
+  if (host_out) o += al(kHdrBytes + 8 * s.C + 2ull * kChunkBytes * s.C);
+  L.total = o;
+  return L;
+}
+
+bool is_device_ptr(const void* p) {
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+}
+
+struct DevInfo {
+  int dev = -1, sms = 0;
+  int occ_sweep2 = 0, occ_sweep3 = 0, occ_decode = 0;
+  bool attrs = false;
+};
+DevInfo g_dev;
+
+int dev_info(DevInfo*& out) {
+  int dev;
+  CK(cudaGetDevice(&dev));
+  if (g_dev.dev != dev || !g_dev.attrs) {
+    g_dev = DevInfo{};
+    g_dev.dev = dev;
+    CK(cudaDeviceGetAttribute(&g_dev.sms, cudaDevAttrMultiProcessorCount, dev));
+    const int smem = (int)sizeof(CodecSmem);
+    CK(cudaFuncSetAttribute(k_encode<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    CK(cudaFuncSetAttribute(k_encode<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    CK(cudaFuncSetAttribute(k_decode, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    CK(cudaFuncSetAttribute(k_quant_repair<float, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)quant_repair_smem<float, 3>()));
+    CK(cudaFuncSetAttribute(k_quant_repair<float, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)quant_repair_smem<float, 2>()));
+    CK(cudaFuncSetAttribute(k_quant_repair<double, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)quant_repair_smem<double, 3>()));
+    CK(cudaFuncSetAttribute(k_quant_repair<double, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)quant_repair_smem<double, 2>()));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_dev.occ_sweep2, k_sweep<2>, kRepairThreads, 0));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_dev.occ_sweep3, k_sweep<3>, kRepairThreads, 0));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_dev.occ_decode, k_decode, kCodecThreads, smem));
+    g_dev.attrs = true;
+  }
+  out = &g_dev;
+  return LOPC_OK;
+}
+
+// pinned status block for the single D2H read per call
+Counters* g_host_ctr = nullptr;
+int host_ctr(Counters*& h) {
+  if (!g_host_ctr) CK(cudaMallocHost(&g_host_ctr, sizeof(Counters)));
+  h = g_host_ctr;
+  return LOPC_OK;
+}
+
+struct Timer {
+  cudaEvent_t ev[8] = {};
+  int n = 0;
+  bool on = false;
+  cudaStream_t st = nullptr;
+  int init(cudaStream_t s) {
+    st = s;
+    on = g_timing != 0;
+    if (!on) return LOPC_OK;
+    for (int i = 0; i < 8; ++i) CK(cudaEventCreate(&ev[i]));
+    return LOPC_OK;
+  }
+  void mark() {
+    if (on && n < 8) cudaEventRecord(ev[n++], st);
+  }
+  float ms(int a, int b) {
+    float v = 0;
+    if (on && b < n) cudaEventElapsedTime(&v, ev[a], ev[b]);
+    return v;
+  }
+  ~Timer() {
+    if (on)
+      for (int i = 0; i < 8; ++i)
+        if (ev[i]) cudaEventDestroy(ev[i]);
+  }
+};
+
+int map_err(uint32_t e) {
+  if (e & kErrVersion) return LOPC_E_VERSION;
+  if (e & kErrCorrupt) return LOPC_E_CORRUPT;
+  if (e & kErrNoSpace) return LOPC_E_NOSPACE;
+  if (e & (kErrBound | kErrOverflow | kErrPassCap)) return LOPC_E_INTERNAL;
+  return LOPC_OK;
+}
+
+void write_header_host(uint8_t* h, const Shape& s, double eps, uint64_t total) {
+  memset(h, 0, kHdrBytes);
+  memcpy(h, "LOPC", 4);
+  uint16_t ver = 1;
+  memcpy(h + 4, &ver, 2);
+  h[6] = (uint8_t)s.dtype;
+  h[7] = (uint8_t)s.ndims;
+  memcpy(h + 8, &s.d0, 8);
+  memcpy(h + 16, &s.d1, 8);
+  memcpy(h + 24, &s.d2, 8);
+  memcpy(h + 32, &eps, 8);
+  memcpy(h + 40, &s.n, 8);
+  uint32_t cb = kChunkBytes, C = (uint32_t)s.C;
+  memcpy(h + 48, &cb, 4);
+  memcpy(h + 52, &C, 4);
+  memcpy(h + 56, &total, 8);
+}
+
+// Steps a1-a3 (quantize, flags, repair to the fixpoint) on device input.
+int run_repair(const Shape& sh, const void* x, double eps, uint8_t* ws, const CLayout& L, cudaStream_t st, Timer& tm,
+               Counters* hc) {
+  DevInfo* di;
+  int rc = dev_info(di);
+  if (rc) return rc;
+  RepairArgs ra{};
+  ra.x = x;
+  ra.flags = ws + L.flags;
+  ra.s = reinterpret_cast<uint32_t*>(ws + L.s);
+  ra.stamp = reinterpret_cast<uint32_t*>(ws + L.stamp);
+  ra.lists = reinterpret_cast<uint32_t*>(ws + L.lists);
+  ra.ctr = reinterpret_cast<Counters*>(ws + L.ctr);
+  ra.eps = eps;
+  ra.inv = 1.0 / eps;
+  ra.d0 = (int64_t)sh.d0;
+  ra.d1 = (int64_t)sh.d1;
+  ra.d2 = (int64_t)sh.d2;
+  ra.ntz = L.ntz;
+  ra.nty = L.nty;
+  ra.ntx = L.ntx;
+  ra.ntiles = (int64_t)L.ntiles;
+  ra.max_inner = 64;
+  ra.max_passes = 1 << 20;
+  const unsigned nt = (unsigned)L.ntiles;
+  if (sh.dtype == LOPC_F32) {
+    if (sh.ndims == 3)
+      k_quant_repair<float, 3><<<nt, kRepairThreads, quant_repair_smem<float, 3>(), st>>>(ra);
+    else
+      k_quant_repair<float, 2><<<nt, kRepairThreads, quant_repair_smem<float, 2>(), st>>>(ra);
+  } else {
+    if (sh.ndims == 3)
+      k_quant_repair<double, 3><<<nt, kRepairThreads, quant_repair_smem<double, 3>(), st>>>(ra);
+    else
+      k_quant_repair<double, 2><<<nt, kRepairThreads, quant_repair_smem<double, 2>(), st>>>(ra);
+  }
+  CK(cudaGetLastError());
+  tm.mark();
+  int occ = sh.ndims == 3 ? di->occ_sweep3 : di->occ_sweep2;
+  uint64_t grid = (uint64_t)occ * di->sms;
+  if (grid > L.ntiles) grid = L.ntiles;
+  if (grid < 1) grid = 1;
+  void* kargs[] = {&ra};
+  if (sh.ndims == 3)
+    CK(cudaLaunchCooperativeKernel((void*)k_sweep<3>, dim3((unsigned)grid), dim3(kRepairThreads), kargs, 0, st));
+  else
+    CK(cudaLaunchCooperativeKernel((void*)k_sweep<2>, dim3((unsigned)grid), dim3(kRepairThreads), kargs, 0, st));
+  tm.mark();
+  (void)hc;
+  return LOPC_OK;
+}
+
+int workspace_for(size_t need, void*& ws, size_t& ws_bytes) {
+  static void* pool = nullptr;
+  static size_t pool_size = 0;
+  static int pool_dev = -1;
+  int dev;
+  CK(cudaGetDevice(&dev));
+  if (pool && (pool_size < need || pool_dev != dev)) {
+    cudaFree(pool);
+    pool = nullptr;
+    pool_size = 0;
+  }
+  if (!pool) {
+    size_t sz = need < (1u << 20) ? (1u << 20) : need;
+    CK(cudaMalloc(&pool, sz));
+    pool_size = sz;
+    pool_dev = dev;
+  }
+  ws = pool;
+  ws_bytes = pool_size;
+  return LOPC_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int lopc_abi_version(void) { return LOPC_ABI_VERSION; }
+
+const char* lopc_strerror(int code) {
+  switch (code) {
+    case LOPC_OK: return "ok";
+    case LOPC_E_ARG: return "invalid argument";
+    case LOPC_E_SHAPE: return "invalid shape";
+    case LOPC_E_NOSPACE: return "output or workspace too small";
+    case LOPC_E_CORRUPT: return "corrupt stream";
+    case LOPC_E_VERSION: return "unsupported stream version";
+    case LOPC_E_CUDA: return "CUDA error";
+    case LOPC_E_NCCL: return "NCCL error";
+    case LOPC_E_INTERNAL: return "internal self-check failed";
+    default: return "unknown error";
+  }
+}
+
+const char* lopc_last_error_string(void) { return g_errmsg; }
+
+void lopc_set_timing(int enable) { g_timing = enable; }
+
+int lopc_last_stats(lopc_stats* out) {
+  if (!out) return LOPC_E_ARG;
+  *out = g_stats;
+  return LOPC_OK;
+}
+
+size_t lopc_compress_bound(int ndims, const uint64_t* dims, int dtype) {
+  Shape s;
+  if (make_shape(ndims, dims, dtype, s)) return 0;
+  return kHdrBytes + 8 * s.C + 2ull * kChunkBytes * s.C;
+}
+
+size_t lopc_compress_workspace_bytes(int ndims, const uint64_t* dims, int dtype, int host_io) {
+  Shape s;
+  if (make_shape(ndims, dims, dtype, s)) return 0;
+  return compress_layout(s, host_io != 0, host_io != 0).total;
+}
+
+size_t lopc_decompress_workspace_bytes(size_t in_bytes, size_t out_bytes, int host_io) {
+  size_t cmax = in_bytes > kHdrBytes ? (in_bytes - kHdrBytes) / 16 + 1 : 1;
+  size_t t = al(sizeof(Counters)) + al(8 * cmax);
+  if (host_io) t += al(in_bytes) + al(out_bytes);
+  return t;
+}
+
+int lopc_stream_info(const void* host_hdr, size_t n, int* ndims, uint64_t* dims3, int* dtype, double* eps,
+                     uint64_t* n_elems, uint32_t* n_chunks) {
+  if (!host_hdr) return LOPC_E_ARG;
+  if (n < kHdrBytes) return LOPC_E_CORRUPT;
+  const uint8_t* h = static_cast<const uint8_t*>(host_hdr);
+  if (memcmp(h, "LOPC", 4) != 0) return LOPC_E_CORRUPT;
+  uint16_t ver;
+  memcpy(&ver, h + 4, 2);
+  if (ver != 1) return LOPC_E_VERSION;
+  int dt = h[6], nd = h[7];
+  if (dt > 1 || (nd != 2 && nd != 3)) return LOPC_E_CORRUPT;
+  uint64_t d[3], nn;
+  double e;
+  uint32_t C;
+  memcpy(d, h + 8, 24);
+  memcpy(&e, h + 32, 8);
+  memcpy(&nn, h + 40, 8);
+  memcpy(&C, h + 52, 4);
+  if (nd == 2 && d[0] != 1) return LOPC_E_CORRUPT;
+  if (ndims) *ndims = nd;
+  if (dims3) memcpy(dims3, d, 24);
+  if (dtype) *dtype = dt;
+  if (eps) *eps = e;
+  if (n_elems) *n_elems = nn;
+  if (n_chunks) *n_chunks = C;
+  return LOPC_OK;
+}
+
+int lopc_compress_ex(const void* in, int ndims, const uint64_t* dims, int dtype, double eps, void* out,
+                     size_t* out_bytes, void* workspace, size_t workspace_bytes, void* stream) {
+  if (!out_bytes || !out || (!in)) return LOPC_E_ARG;
+  Shape sh;
+  int rc = make_shape(ndims, dims, dtype, sh);
+  if (rc) return rc;
+  if ((rc = check_eps(eps))) return rc;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const bool host_in = !is_device_ptr(in), host_out = !is_device_ptr(out);
+  const size_t cap = *out_bytes;
+  g_stats = lopc_stats{};
+  g_stats.n_elems = sh.n;
+  g_stats.n_chunks = sh.C;
+  if (sh.n == 0) {
+    if (cap < kHdrBytes) {
+      *out_bytes = kHdrBytes;
+      return LOPC_E_NOSPACE;
+    }
+    uint8_t h[kHdrBytes];
+    write_header_host(h, sh, eps, kHdrBytes);
+    if (host_out)
+      memcpy(out, h, kHdrBytes);
+    else {
+      CK(cudaMemcpyAsync(out, h, kHdrBytes, cudaMemcpyHostToDevice, st));
+      CK(cudaStreamSynchronize(st));
+    }
+    *out_bytes = kHdrBytes;
+    g_stats.total_bytes = kHdrBytes;
+    return LOPC_OK;
+  }
+  const CLayout L = compress_layout(sh, host_in, host_out);
+  if (!workspace || workspace_bytes < L.total) return LOPC_E_NOSPACE;
+  uint8_t* ws = static_cast<uint8_t*>(workspace);
+  g_stats.n_tiles = L.ntiles;
+  Counters* hc;
+  if ((rc = host_ctr(hc))) return rc;
+  DevInfo* di;
+  if ((rc = dev_info(di))) return rc;
+  Timer tm;
+  if ((rc = tm.init(st))) return rc;
+  tm.mark();  // 0
+  const void* x = in;
+  if (host_in) {
+    CK(cudaMemcpyAsync(ws + L.stage_in, in, sh.k * sh.n, cudaMemcpyHostToDevice, st));
+    x = ws + L.stage_in;
+  }
+  tm.mark();  // 1
+  CK(cudaMemsetAsync(ws, 0, L.zero_end, st));
+  if ((rc = run_repair(sh, x, eps, ws, L, st, tm, hc))) return rc;  // marks 2, 3
+  uint8_t* dst = host_out ? ws + L.stage_out : static_cast<uint8_t*>(out);
+  EncodeArgs ea{};
+  ea.x = x;
+  ea.s = reinterpret_cast<const uint32_t*>(ws + L.s);
+  ea.out = dst;
+  ea.out_cap = host_out ? (kHdrBytes + 8 * sh.C + 2ull * kChunkBytes * sh.C) : cap;
+  ea.state = reinterpret_cast<uint64_t*>(ws + L.state);
+  ea.ctr = reinterpret_cast<Counters*>(ws + L.ctr);
+  ea.eps = eps;
+  ea.inv = 1.0 / eps;
+  ea.n = sh.n;
+  ea.C = (uint32_t)sh.C;
+  ea.ndims = sh.ndims;
+  ea.d0 = sh.d0;
+  ea.d1 = sh.d1;
+  ea.d2 = sh.d2;
+  const size_t smem = sizeof(CodecSmem);
+  if (sh.dtype == LOPC_F32)
+    k_encode<float><<<(unsigned)sh.C, kCodecThreads, smem, st>>>(ea);
+  else
+    k_encode<double><<<(unsigned)sh.C, kCodecThreads, smem, st>>>(ea);
+  CK(cudaGetLastError());
+  tm.mark();  // 4
+  CK(cudaMemcpyAsync(hc, ws + L.ctr, sizeof(Counters), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  const uint64_t total = hc->total_bytes;
+  g_stats.sweep_passes = hc->passes;
+  g_stats.tiles_processed = hc->tiles_processed;
+  g_stats.inner_iters = hc->inner_iters;
+  g_stats.escapes = hc->escapes;
+  g_stats.bin_bytes = hc->bin_bytes;
+  g_stats.sub_bytes = hc->sub_bytes;
+  g_stats.total_bytes = total;
+  g_stats.max_subbin = hc->max_s;
+  uint32_t err = hc->err;
+  if (hc->list_count[(hc->passes + 1) % 3] != 0 && hc->passes >= (1ull << 20)) err |= kErrPassCap;
+  if ((rc = map_err(err & ~kErrNoSpace))) return rc;
+  if (total > cap) {
+    *out_bytes = total;
+    return LOPC_E_NOSPACE;
+  }
+  if (host_out) {
+    CK(cudaMemcpyAsync(out, dst, total, cudaMemcpyDeviceToHost, st));
+  }
+  tm.mark();  // 5
+  CK(cudaStreamSynchronize(st));
+  *out_bytes = total;
+  if (tm.on) {
+    g_stats.timing_valid = 1;
+    g_stats.ms_h2d = tm.ms(0, 1);
+    g_stats.ms_quant_repair = tm.ms(1, 2);
+    g_stats.ms_sweep = tm.ms(2, 3);
+    g_stats.ms_encode = tm.ms(3, 4);
+    g_stats.ms_d2h = tm.ms(4, 5);
+    g_stats.ms_total = tm.ms(0, 5);
+  }
+  return LOPC_OK;
+}
+
+int lopc_compress(const void* in, int ndims, const uint64_t* dims, int dtype, double eps, void* out,
+                  size_t* out_bytes) {
+  size_t need = lopc_compress_workspace_bytes(ndims, dims, dtype, 1);
+  if (need == 0) {
+    Shape s;
+    int rc = make_shape(ndims, dims, dtype, s);
+    return rc ? rc : LOPC_E_ARG;
+  }
+  void* ws;
+  size_t wsb;
+  int rc = workspace_for(need, ws, wsb);
+  if (rc) return rc;
+  return lopc_compress_ex(in, ndims, dims, dtype, eps, out, out_bytes, ws, wsb, nullptr);
+}
+
+int lopc_repair_ex(const void* in, int ndims, const uint64_t* dims, int dtype, double eps, uint16_t* flags_out,
+                   uint32_t* subbins_out, void* workspace, size_t workspace_bytes, void* stream) {
+  if (!in) return LOPC_E_ARG;
+  Shape sh;
+  int rc = make_shape(ndims, dims, dtype, sh);
+  if (rc) return rc;
+  if ((rc = check_eps(eps))) return rc;
+  if (sh.n == 0) return LOPC_OK;
+  if (!is_device_ptr(in)) return LOPC_E_ARG;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const CLayout L = compress_layout(sh, false, false);
+  if (!workspace || workspace_bytes < L.total) return LOPC_E_NOSPACE;
+  uint8_t* ws = static_cast<uint8_t*>(workspace);
+  Counters* hc;
+  if ((rc = host_ctr(hc))) return rc;
+  Timer tm;
+  CK(cudaMemsetAsync(ws, 0, L.zero_end, st));
+  if ((rc = run_repair(sh, in, eps, ws, L, st, tm, hc))) return rc;
+  if (subbins_out) CK(cudaMemcpyAsync(subbins_out, ws + L.s, 4 * sh.n, cudaMemcpyDeviceToDevice, st));
+  if (flags_out) {
+    if (sh.ndims == 3) {
+      CK(cudaMemcpyAsync(flags_out, ws + L.flags, 2 * sh.n, cudaMemcpyDeviceToDevice, st));
+    } else {
+      // widen u8 -> u16 with a strided 2D copy into the low bytes
+      CK(cudaMemsetAsync(flags_out, 0, 2 * sh.n, st));
+      CK(cudaMemcpy2DAsync(flags_out, 2, ws + L.flags, 1, 1, sh.n, cudaMemcpyDeviceToDevice, st));
+    }
+  }
+  CK(cudaMemcpyAsync(hc, ws + L.ctr, sizeof(Counters), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  g_stats = lopc_stats{};
+  g_stats.n_elems = sh.n;
+  g_stats.n_tiles = L.ntiles;
+  g_stats.sweep_passes = hc->passes;
+  g_stats.tiles_processed = hc->tiles_processed;
+  g_stats.inner_iters = hc->inner_iters;
+  g_stats.max_subbin = hc->max_s;
+  return map_err(hc->err);
+}
+
+int lopc_decompress_ex(const void* in, size_t in_bytes, void* out, size_t out_capacity, void* workspace,
+                       size_t workspace_bytes, void* stream) {
+  if (!in || !out) return LOPC_E_ARG;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const bool host_in = !is_device_ptr(in), host_out = !is_device_ptr(out);
+  const size_t cmax = in_bytes > kHdrBytes ? (in_bytes - kHdrBytes) / 16 + 1 : 1;
+  size_t o_ctr = 0, o_state = al(sizeof(Counters)), o_in = o_state + al(8 * cmax);
+  size_t o_out = o_in + (host_in ? al(in_bytes) : 0);
+  size_t need = o_out + (host_out ? al(out_capacity) : 0);
+  if (!workspace || workspace_bytes < need) return LOPC_E_NOSPACE;
+  uint8_t* ws = static_cast<uint8_t*>(workspace);
+  int rc;
+  Counters* hc;
+  if ((rc = host_ctr(hc))) return rc;
+  DevInfo* di;
+  if ((rc = dev_info(di))) return rc;
+  Timer tm;
+  if ((rc = tm.init(st))) return rc;
+  g_stats = lopc_stats{};
+  tm.mark();  // 0
+  const uint8_t* src = static_cast<const uint8_t*>(in);
+  if (host_in) {
+    CK(cudaMemcpyAsync(ws + o_in, in, in_bytes, cudaMemcpyHostToDevice, st));
+    src = ws + o_in;
+  }
+  tm.mark();  // 1
+  CK(cudaMemsetAsync(ws, 0, o_in, st));
+  DecodeArgs da{};
+  da.in = src;
+  da.in_bytes = in_bytes;
+  da.out = host_out ? (void*)(ws + o_out) : out;
+  da.out_cap = out_capacity;
+  da.state = reinterpret_cast<uint64_t*>(ws + o_state);
+  da.state_cap = cmax;
+  da.ctr = reinterpret_cast<Counters*>(ws + o_ctr);
+  unsigned grid = (unsigned)(di->occ_decode * di->sms);
+  if (grid > cmax) grid = (unsigned)cmax;
+  if (grid < 1) grid = 1;
+  k_decode<<<grid, kCodecThreads, sizeof(CodecSmem), st>>>(da);
+  CK(cudaGetLastError());
+  tm.mark();  // 2
+  CK(cudaMemcpyAsync(hc, ws + o_ctr, sizeof(Counters), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if ((rc = map_err(hc->err))) return rc;
+  if (host_out) {
+    // N * k from the (validated) header
+    uint64_t nk = 0;
+    uint8_t h[kHdrBytes];
+    if (host_in)
+      memcpy(h, in, kHdrBytes);
+    else
+      CK(cudaMemcpy(h, in, kHdrBytes, cudaMemcpyDeviceToHost));
+    uint64_t n;
+    memcpy(&n, h + 40, 8);
+    nk = n * (h[6] ? 8 : 4);
+    CK(cudaMemcpyAsync(out, ws + o_out, nk, cudaMemcpyDeviceToHost, st));
+  }
+  tm.mark();  // 3
+  CK(cudaStreamSynchronize(st));
+  if (tm.on) {
+    g_stats.timing_valid = 1;
+    g_stats.ms_h2d = tm.ms(0, 1);
+    g_stats.ms_decode = tm.ms(1, 2);
+    g_stats.ms_d2h = tm.ms(2, 3);
+    g_stats.ms_total = tm.ms(0, 3);
+  }
+  return LOPC_OK;
+}
+
+int lopc_decompress(const void* in, size_t in_bytes, void* out, size_t out_capacity) {
+  size_t need = lopc_decompress_workspace_bytes(in_bytes, out_capacity, 1);
+  void* ws;
+  size_t wsb;
+  int rc = workspace_for(need, ws, wsb);
+  if (rc) return rc;
+  return lopc_decompress_ex(in, in_bytes, out, out_capacity, ws, wsb, nullptr);
+}
+
+}  // extern "C"

@@ -1,0 +1,150 @@
+// lopc_device.cuh — device primitives of the LOPC hot path (sm_100a).
+//
+// Product code.  Shares nothing with the CPU reference implementation: the two are
+// written independently from PAPER.md and DESIGN.md §3-§4 and compared only
+// through their outputs.
+//
+// Compiled with -fmad=false: no FMA contraction anywhere; __fma_rn is used
+// explicitly only for the TwoProduct error term of lo().
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace lopc {
+
+constexpr uint32_t kChunkBytes = 16384;  // "16kB chunks" (G22)
+constexpr uint32_t kHdrBytes = 64;
+
+// Value-type traits: word width k, bin/ord integer types, escape sentinel
+// (G10), BINMAX (G8).
+template <typename T>
+struct VT;
+template <>
+struct VT<float> {
+  using U = uint32_t;  // raw bits / stream word
+  using I = int32_t;   // bin and ord
+  static constexpr int K = 4;
+  static constexpr U kSentinel = 0x80000000u;
+  static constexpr double kBinMax = 2147483646.0;
+};
+template <>
+struct VT<double> {
+  using U = uint64_t;
+  using I = int64_t;
+  static constexpr int K = 8;
+  static constexpr U kSentinel = 0x8000000000000000ull;
+  static constexpr double kBinMax = 1125899906842624.0;
+};
+
+__host__ __device__ __forceinline__ uint32_t as_bits(float v) {
+#ifdef __CUDA_ARCH__
+  return __float_as_uint(v);
+#else
+  uint32_t u;
+  __builtin_memcpy(&u, &v, 4);
+  return u;
+#endif
+}
+__host__ __device__ __forceinline__ uint64_t as_bits(double v) {
+#ifdef __CUDA_ARCH__
+  return (uint64_t)__double_as_longlong(v);
+#else
+  uint64_t u;
+  __builtin_memcpy(&u, &v, 8);
+  return u;
+#endif
+}
+
+// SoS value key: monotone map of the bit pattern to an integer,
+// -0.0 and +0.0 both map to 0 (G13).
+__device__ __forceinline__ int32_t key_of(uint32_t u) {
+  int32_t i = (int32_t)u;
+  return i >= 0 ? i : -(int32_t)(u & 0x7fffffffu);
+}
+__device__ __forceinline__ int64_t key_of(uint64_t u) {
+  int64_t i = (int64_t)u;
+  return i >= 0 ? i : -(int64_t)(u & 0x7fffffffffffffffull);
+}
+__device__ __forceinline__ uint32_t bits_of_key32(int64_t o) {
+  return o >= 0 ? (uint32_t)o : (0x80000000u | (uint32_t)(-o));
+}
+__device__ __forceinline__ uint64_t bits_of_key64(int64_t o) {
+  return o >= 0 ? (uint64_t)o : (0x8000000000000000ull | (uint64_t)(-o));
+}
+
+// 1.5 * 2^52: adding it rounds a double of magnitude < 2^51 to an integer
+// held in the low mantissa bits (no F2I/I2F conversions needed).
+constexpr double kMagic = 6755399441055744.0;
+
+__device__ __forceinline__ double i64_to_f64_exact(int64_t b) {
+  // exact for |b| < 2^51
+  return __longlong_as_double(__double_as_longlong(kMagic) + b) - kMagic;
+}
+
+// lo(b): the smallest dtype value >= (b - 1/2) * eps, exactly ("subbin 0
+// decodes to the lowest representable value within the bin"; G7).
+// a = b - 1/2 is exact; a*eps = p + e exactly with e = fma(a, eps, -p).
+__device__ __forceinline__ float lo_f32(int64_t b, double eps) {
+  double a = i64_to_f64_exact(b) - 0.5;
+  double p = __dmul_rn(a, eps);
+  double e = __fma_rn(a, eps, -p);
+  float f = __double2float_ru(p);  // smallest float >= p
+  if (e > 0.0 && (double)f == p) f = __uint_as_float(bits_of_key32((int64_t)key_of(__float_as_uint(f)) + 1));
+  return f;
+}
+__device__ __forceinline__ double lo_f64(int64_t b, double eps) {
+  double a = i64_to_f64_exact(b) - 0.5;
+  double p = __dmul_rn(a, eps);
+  double e = __fma_rn(a, eps, -p);
+  if (e > 0.0) p = __longlong_as_double((long long)bits_of_key64(key_of((uint64_t)__double_as_longlong(p)) + 1));
+  return p;
+}
+template <typename T>
+__device__ __forceinline__ T lo_t(int64_t b, double eps);
+template <>
+__device__ __forceinline__ float lo_t<float>(int64_t b, double eps) { return lo_f32(b, eps); }
+template <>
+__device__ __forceinline__ double lo_t<double>(int64_t b, double eps) { return lo_f64(b, eps); }
+
+// Exact bin b = floor(x/eps + 1/2) (P:114 with reading G6) and the
+// double-check of the north star: returns false (escape) for non-finite x or
+// |b| > BINMAX (G8/G9).
+//
+// t = RN(x * RN(1/eps)) differs from x/eps by less than |t| 2^-51.  If t is
+// farther than that from a half-integer, b = rint(t) is proven exact;
+// otherwise b is fixed up by the exact interval test lo(b) <= x < lo(b+1)
+// (one step suffices: |t - x/eps| < 1/4 whenever |t| <= 2^51).
+template <typename T>
+__device__ __forceinline__ bool quantize(T x, double eps, double inv, typename VT<T>::I& bout) {
+  using I = typename VT<T>::I;
+  double xd = (double)x;
+  double t = xd * inv;
+  // NaN/Inf fail the compare; |t| > 2 BINMAX certainly means |b| > BINMAX
+  if (!(fabs(t) <= 2.0 * VT<T>::kBinMax)) return false;
+  double tm = t + kMagic;
+  int64_t r = __double_as_longlong(tm) - __double_as_longlong(kMagic);
+  double rd = tm - kMagic;
+  double d = fabs(t - rd);
+  double margin = 0.5 - fabs(t) * 0x1p-50 - 0x1p-60;
+  if (!(d < margin)) {
+    if (xd < (double)lo_t<T>(r, eps))
+      r -= 1;
+    else if (xd >= (double)lo_t<T>(r + 1, eps))
+      r += 1;
+  }
+  if (r > (int64_t)VT<T>::kBinMax || r < -(int64_t)VT<T>::kBinMax) return false;
+  bout = (I)r;
+  return true;
+}
+
+// ---- memory-model helpers ------------------------------------------------
+__device__ __forceinline__ uint64_t ld_acquire_u64(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_u64(uint64_t* p, uint64_t v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+}  // namespace lopc

@@ -1,0 +1,209 @@
+"""Thin ctypes binding of liblopc.so (include/lopc.h).
+
+Argument marshalling only: every step of the hot path runs in the CUDA
+kernels of ``csrc/``.  PyTorch provides device memory (workspaces, outputs)
+and the current CUDA stream.  There is no CPU fallback: if ``liblopc.so`` is
+missing or no GPU is visible, every call raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import re
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+SO = os.path.join(_HERE, "liblopc.so")
+HEADER = os.path.join(os.path.dirname(_HERE), "include", "lopc.h")
+
+F32, F64 = 0, 1
+ERRORS = {0: "OK", -1: "E_ARG", -2: "E_SHAPE", -3: "E_NOSPACE", -4: "E_CORRUPT", -5: "E_VERSION",
+          -6: "E_CUDA", -7: "E_NCCL", -8: "E_INTERNAL"}
+
+
+class LopcError(RuntimeError):
+    def __init__(self, code: int, what: str, detail: str = ""):
+        msg = f"{what}: {ERRORS.get(code, code)}"
+        if detail:
+            msg += f" ({detail})"
+        super().__init__(msg)
+        self.code = code
+
+
+class Stats(C.Structure):
+    _fields_ = [(n, C.c_uint64) for n in ("n_elems", "n_chunks", "n_tiles", "sweep_passes", "tiles_processed",
+                                          "inner_iters", "escapes", "bin_bytes", "sub_bytes", "total_bytes")] + [
+        ("max_subbin", C.c_uint32), ("timing_valid", C.c_uint32)] + [
+        (n, C.c_float) for n in ("ms_h2d", "ms_quant_repair", "ms_sweep", "ms_encode", "ms_decode", "ms_d2h",
+                                 "ms_total")]
+
+
+_lib = None
+
+
+def declared_symbols() -> list[str]:
+    """Function names declared in include/lopc.h."""
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(lopc_[a-z0-9_]+)\s*\(", src)))
+
+
+def load(require_gpu: bool = True):
+    """Load liblopc.so (raises if it is missing; with require_gpu, also if no
+    CUDA device is visible)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(SO):
+            raise ImportError(f"{SO} is missing: run __graft_entry__.build() (nvcc, sm_100a)")
+        L = C.CDLL(SO)
+        P, I, D, SZ, U64P = C.c_void_p, C.c_int, C.c_double, C.c_size_t, C.POINTER(C.c_uint64)
+        L.lopc_compress_bound.argtypes = [I, U64P, I]
+        L.lopc_compress_bound.restype = SZ
+        L.lopc_compress_workspace_bytes.argtypes = [I, U64P, I, I]
+        L.lopc_compress_workspace_bytes.restype = SZ
+        L.lopc_decompress_workspace_bytes.argtypes = [SZ, SZ, I]
+        L.lopc_decompress_workspace_bytes.restype = SZ
+        L.lopc_compress.argtypes = [P, I, U64P, I, D, P, C.POINTER(SZ)]
+        L.lopc_compress_ex.argtypes = [P, I, U64P, I, D, P, C.POINTER(SZ), P, SZ, P]
+        L.lopc_decompress.argtypes = [P, SZ, P, SZ]
+        L.lopc_decompress_ex.argtypes = [P, SZ, P, SZ, P, SZ, P]
+        L.lopc_repair_ex.argtypes = [P, I, U64P, I, D, P, P, P, SZ, P]
+        L.lopc_stream_info.argtypes = [P, SZ, C.POINTER(I), U64P, C.POINTER(I), C.POINTER(D), U64P,
+                                       C.POINTER(C.c_uint32)]
+        L.lopc_last_stats.argtypes = [C.POINTER(Stats)]
+        L.lopc_set_timing.argtypes = [I]
+        L.lopc_set_timing.restype = None
+        L.lopc_strerror.restype = C.c_char_p
+        L.lopc_last_error_string.restype = C.c_char_p
+        for f in ("lopc_compress", "lopc_compress_ex", "lopc_decompress", "lopc_decompress_ex", "lopc_repair_ex",
+                  "lopc_stream_info", "lopc_last_stats", "lopc_abi_version"):
+            getattr(L, f).restype = I
+        _lib = L
+    if require_gpu and not torch.cuda.is_available():
+        raise RuntimeError("liblopc needs a CUDA GPU (B200); there is no CPU fallback")
+    return _lib
+
+
+def _dims(shape):
+    return (C.c_uint64 * 3)(*([int(v) for v in shape] + [0] * (3 - len(shape))))
+
+
+def _dtype_code(dt) -> int:
+    if dt == torch.float32:
+        return F32
+    if dt == torch.float64:
+        return F64
+    raise TypeError(f"LOPC compresses float32/float64 grids, got {dt}")
+
+
+def _check(rc: int, what: str):
+    if rc != 0:
+        raise LopcError(rc, what, load(False).lopc_last_error_string().decode())
+
+
+_ws = {}
+
+
+def _workspace(nbytes: int, device) -> torch.Tensor:
+    key = torch.device(device).index if torch.device(device).type == "cuda" else torch.cuda.current_device()
+    t = _ws.get(key)
+    if t is None or t.numel() < nbytes:
+        t = torch.empty(max(nbytes, 1 << 20), dtype=torch.uint8, device=f"cuda:{key}")
+        _ws[key] = t
+    return t
+
+
+def _stream(device=None):
+    return C.c_void_p(torch.cuda.current_stream(device).cuda_stream)
+
+
+def compress_bound(shape, dtype) -> int:
+    return int(load(False).lopc_compress_bound(len(shape), _dims(shape), _dtype_code(dtype)))
+
+
+def compress(x: torch.Tensor, eps: float, out: torch.Tensor | None = None) -> torch.Tensor:
+    """lopc_compress_ex on x (2D/3D float32/float64, device or host memory).
+    Returns a uint8 tensor view of exactly the stream bytes (on ``out``'s
+    device/host memory if given, else on x's device; host x -> host out)."""
+    L = load()
+    if x.dim() not in (2, 3):
+        raise ValueError("x must be 2D or 3D")
+    x = x.contiguous()
+    dev = x.device if x.is_cuda else torch.device("cuda", torch.cuda.current_device())
+    cap = compress_bound(x.shape, x.dtype)
+    if out is None:
+        out = torch.empty(cap, dtype=torch.uint8, device=x.device)
+    host_io = int((not x.is_cuda) or (not out.is_cuda))
+    need = L.lopc_compress_workspace_bytes(x.dim(), _dims(x.shape), _dtype_code(x.dtype), host_io)
+    ws = _workspace(need, dev)
+    nbytes = C.c_size_t(out.numel())
+    with torch.cuda.device(dev):
+        rc = L.lopc_compress_ex(C.c_void_p(x.data_ptr()), x.dim(), _dims(x.shape), _dtype_code(x.dtype),
+                                float(eps), C.c_void_p(out.data_ptr()), C.byref(nbytes),
+                                C.c_void_p(ws.data_ptr()), ws.numel(), _stream(dev))
+    _check(rc, "lopc_compress")
+    return out[: nbytes.value]
+
+
+def stream_info(stream: torch.Tensor) -> dict:
+    hdr = stream[:64].cpu().numpy().tobytes() if stream.numel() >= 64 else bytes(stream.cpu().numpy())
+    buf = C.create_string_buffer(hdr, len(hdr))
+    nd, dt, e = C.c_int(), C.c_int(), C.c_double()
+    d3 = (C.c_uint64 * 3)()
+    n, c = C.c_uint64(), C.c_uint32()
+    rc = load(False).lopc_stream_info(buf, len(hdr), C.byref(nd), d3, C.byref(dt), C.byref(e), C.byref(n), C.byref(c))
+    _check(rc, "lopc_stream_info")
+    dims = tuple(int(v) for v in d3)
+    shape = dims[1:] if nd.value == 2 else dims
+    return {"ndims": nd.value, "shape": shape, "dtype": torch.float32 if dt.value == 0 else torch.float64,
+            "eps": e.value, "n": n.value, "chunks": c.value}
+
+
+def decompress(stream: torch.Tensor, out: torch.Tensor | None = None, info: dict | None = None) -> torch.Tensor:
+    """lopc_decompress_ex.  ``stream`` may live on the device or the host; the
+    result is allocated on the stream's device (or on ``out``)."""
+    L = load()
+    stream = stream.contiguous()
+    if out is None:
+        info = info or stream_info(stream)
+        dev = stream.device if stream.is_cuda else torch.device("cuda", torch.cuda.current_device())
+        out = torch.empty(info["shape"], dtype=info["dtype"], device=dev)
+    dev = out.device if out.is_cuda else (stream.device if stream.is_cuda else
+                                          torch.device("cuda", torch.cuda.current_device()))
+    host_io = int((not stream.is_cuda) or (not out.is_cuda))
+    nb = out.numel() * out.element_size()
+    need = L.lopc_decompress_workspace_bytes(stream.numel(), nb, host_io)
+    ws = _workspace(need, dev)
+    with torch.cuda.device(dev):
+        rc = L.lopc_decompress_ex(C.c_void_p(stream.data_ptr()), stream.numel(), C.c_void_p(out.data_ptr()), nb,
+                                  C.c_void_p(ws.data_ptr()), ws.numel(), _stream(dev))
+    _check(rc, "lopc_decompress")
+    return out
+
+
+def repair(x: torch.Tensor, eps: float):
+    """Steps a1-a3 only: returns (flags u16 as int16, subbins u32 as int32),
+    both device tensors shaped like x."""
+    L = load()
+    x = x.contiguous()
+    flags = torch.empty(x.shape, dtype=torch.int16, device=x.device)
+    s = torch.empty(x.shape, dtype=torch.int32, device=x.device)
+    need = L.lopc_compress_workspace_bytes(x.dim(), _dims(x.shape), _dtype_code(x.dtype), 0)
+    ws = _workspace(need, x.device)
+    with torch.cuda.device(x.device):
+        rc = L.lopc_repair_ex(C.c_void_p(x.data_ptr()), x.dim(), _dims(x.shape), _dtype_code(x.dtype), float(eps),
+                              C.c_void_p(flags.data_ptr()), C.c_void_p(s.data_ptr()), C.c_void_p(ws.data_ptr()),
+                              ws.numel(), _stream(x.device))
+    _check(rc, "lopc_repair_ex")
+    return flags, s
+
+
+def set_timing(on: bool = True):
+    load(False).lopc_set_timing(1 if on else 0)
+
+
+def last_stats() -> dict:
+    st = Stats()
+    load(False).lopc_last_stats(C.byref(st))
+    return {name: getattr(st, name) for name, _ in Stats._fields_}

@@ -1,0 +1,247 @@
+"""GPU parity: the CUDA path (through the C-ABI, via the ctypes binding)
+against the CPU oracle, element by element / byte by byte, on the same seeded
+inputs.  Bar (BASELINE.json north star): byte-identical streams,
+bit-identical decoded values, identical flags and subbins (all integer or
+bit-level results, so exact equality)."""
+import os
+
+import numpy as np
+import pytest
+
+from synth.fields import CONFIGS, eps_noa, random_field
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def gpu():
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.fail("no CUDA device: -m gpu tests must run on a B200")
+    import paper_2603_26968_b200 as lopc
+
+    lopc.load()
+    return lopc
+
+
+def _t(x, dev="cuda"):
+    import torch
+
+    return torch.from_numpy(np.ascontiguousarray(x)).to(dev)
+
+
+def check_all(ref, gpu, x, eps, repair=True):
+    """Full parity of one field: flags + subbins (a1-a3), stream bytes (a4-a7),
+    decoded bits (a8), both decoders on both streams."""
+    xt = _t(x)
+    if repair and x.size:
+        f, s = gpu.repair(xt, eps)
+        fr = ref.flags(x, eps)
+        sr = ref.subbins(x, eps)
+        assert np.array_equal(f.cpu().numpy().view(np.uint16), fr), "flags differ"
+        assert np.array_equal(s.cpu().numpy().view(np.uint32), sr), "subbins differ"
+    st_gpu = gpu.compress(xt, eps).cpu().numpy().tobytes()
+    st_ref = ref.compress(x, eps)
+    assert len(st_gpu) == len(st_ref)
+    assert st_gpu == st_ref, "stream bytes differ"
+    y_gpu = gpu.decompress(_t(np.frombuffer(st_ref, np.uint8).copy())).cpu().numpy()
+    y_ref = ref.decompress(st_ref)
+    assert y_gpu.tobytes() == y_ref.tobytes(), "decoded bits differ"
+    return st_ref
+
+
+def test_golden_a5_on_gpu(ref, gpu):
+    from tests.test_oracle_fixpoint import load_golden
+
+    rows = load_golden()
+    x = np.array([r[1] for r in rows], np.uint32).view(np.float32).reshape(3, 4)
+    f, s = gpu.repair(_t(x), 0.25)
+    f = f.cpu().numpy().view(np.uint16).ravel()
+    s = s.cpu().numpy().view(np.uint32).ravel()
+    for i, (_, _, b, m, sv, _) in enumerate(rows):
+        assert f[i] == m
+        if b is not None:
+            assert s[i] == sv
+    st = check_all(ref, gpu, x, 0.25)
+    y = gpu.decompress(_t(np.frombuffer(st, np.uint8).copy())).cpu().numpy().view(np.uint32).ravel()
+    assert list(y) == [r[5] for r in rows]
+
+
+SMALL = []
+for seed in range(12):
+    for kind in ("noise", "smooth", "ties", "plateau", "grid16"):
+        SMALL.append((seed, kind))
+
+
+@pytest.mark.parametrize("seed,kind", SMALL)
+def test_random_fields(ref, gpu, seed, kind):
+    """Shapes spanning several tiles (3D tile 8x8x32, 2D 32x64) and chunks
+    (4096 f32 / 2048 f64 words) with ragged tails in every dimension."""
+    rng = np.random.default_rng(500 + seed)
+    if seed % 2:
+        dims = (int(rng.integers(1, 90)), int(rng.integers(1, 200)))
+    else:
+        dims = (int(rng.integers(1, 20)), int(rng.integers(1, 30)), int(rng.integers(1, 80)))
+    dt = "f64" if seed % 3 == 0 else "f32"
+    x = random_field(dims, dt, kind, seed)
+    rel = [1e-1, 1e-2, 1e-3, 1.0][seed % 4]
+    check_all(ref, gpu, x, eps_noa(x, rel))
+
+
+@pytest.mark.parametrize("name", ["cfg1", "cfg2s", "cfg3s", "cfg4s"])
+def test_config_shaped(ref, gpu, name):
+    """The configs' generators at oracle-friendly sizes (cfg1 full size)."""
+    small = {"cfg1": None, "cfg2s": (20, 100, 100), "cfg3s": (64, 64, 64), "cfg4s": (180, 360)}[name]
+    cfg = CONFIGS[name[:4]]
+    x = cfg.generate(small)
+    check_all(ref, gpu, x, eps_noa(x, cfg.rel))
+
+
+def test_long_chains_cross_many_tiles(ref, gpu):
+    """Decreasing ramps in one bin: chains of length n need subbins n-1..0
+     and cross many tiles -> many k_sweep passes and the
+    tile-local iteration cap (self re-enlisting)."""
+    x = (1.0 - 1e-6 * np.arange(6000)).astype(np.float32).reshape(1, 6000)
+    st = check_all(ref, gpu, x, 1.0)
+    assert gpu.last_stats()["total_bytes"] == len(st)
+    x3 = (1.0 - 1e-7 * np.arange(9 * 17 * 70)).astype(np.float32).reshape(9, 17, 70)
+    check_all(ref, gpu, x3, 1.0)
+    x2 = np.full((40, 130), 0.5, np.float32)  # one plateau: all ties -> all zero
+    check_all(ref, gpu, x2, 10.0)
+
+
+def test_escapes_and_edges(ref, gpu):
+    x = random_field((37, 41), "f32", "noise", 8)
+    x.ravel()[[0, 5, 99, 1000]] = [np.nan, np.inf, -np.inf, 3e38]
+    check_all(ref, gpu, x, 1e-3)
+    y = random_field((5, 6, 7), "f64", "noise", 9)
+    y.ravel()[[1, 2]] = [np.nan, 1e300]
+    check_all(ref, gpu, y, 1e-6)
+    for shape in [(1, 1), (1, 4097), (2, 2048), (3, 1, 5), (1, 1, 1)]:
+        check_all(ref, gpu, random_field(shape, "f32", "noise", 1), 0.1)
+    # all-NaN
+    check_all(ref, gpu, np.full((8, 9), np.nan, np.float32), 0.1)
+    # raw fallback both streams
+    r = random_field((64, 128), "f32", "noise", 9) * np.float32(1e6)
+    check_all(ref, gpu, r, 1e-3)
+
+
+def test_empty_input(ref, gpu):
+    import torch
+
+    x = torch.zeros((0, 5), dtype=torch.float32, device="cuda")
+    st = gpu.compress(x, 0.1).cpu().numpy().tobytes()
+    assert st == ref.compress(np.zeros((0, 5), np.float32), 0.1)
+    assert len(st) == 64
+
+
+def test_host_buffers_same_bytes(ref, gpu):
+    """The C-ABI accepts host buffers (staged inside the call): same bytes."""
+    import torch
+
+    x = CONFIGS["cfg4"].generate((90, 300))
+    eps = eps_noa(x, 1e-3)
+    xh = torch.from_numpy(x).pin_memory()
+    out = torch.empty(gpu.compress_bound(x.shape, xh.dtype), dtype=torch.uint8).pin_memory()
+    st = gpu.compress(xh, eps, out=out)
+    assert not st.is_cuda
+    assert st.numpy().tobytes() == ref.compress(x, eps)
+    yh = torch.empty(x.shape, dtype=torch.float32).pin_memory()
+    y = gpu.decompress(st, out=yh)
+    assert y.numpy().tobytes() == ref.decompress(st.numpy().tobytes()).tobytes()
+
+
+def test_corrupt_streams(ref, gpu):
+    import torch
+
+    x = random_field((30, 200), "f32", "smooth", 3)
+    st = ref.compress(x, eps_noa(x, 1e-2))
+
+    def rc_gpu(b):
+        t = torch.from_numpy(np.frombuffer(b, np.uint8).copy()).cuda()
+        out = torch.empty(x.shape, dtype=torch.float32, device="cuda")
+        try:
+            gpu.decompress(t, out=out)
+            return 0
+        except gpu.LopcError as e:
+            return e.code
+
+    assert rc_gpu(st) == 0
+    assert rc_gpu(st[:-4]) == ref.decompress_rc(st[:-4], x.shape, x.dtype) == -4
+    assert rc_gpu(b"XOPC" + st[4:]) == -4
+    v = bytearray(st)
+    v[4] = 2
+    assert rc_gpu(bytes(v)) == -5
+    import struct
+
+    t = bytearray(st)
+    struct.pack_into("<I", t, 64, 8)
+    assert rc_gpu(bytes(t)) == ref.decompress_rc(bytes(t), x.shape, x.dtype) == -4
+    # payload bytes flipped: the GPU must not crash; if the oracle calls it
+    # corrupt the GPU must too
+    rng = np.random.default_rng(0)
+    for _ in range(20):
+        t = bytearray(st)
+        pos = int(rng.integers(64 + 8 * 2, len(st)))
+        t[pos] ^= int(rng.integers(1, 256))
+        r_ref = ref.decompress_rc(bytes(t), x.shape, x.dtype)
+        r_gpu = rc_gpu(bytes(t))
+        assert (r_ref == 0) == (r_gpu == 0), (pos, r_ref, r_gpu)
+
+
+def test_determinism_repeat(ref, gpu):
+    x = CONFIGS["cfg2"].generate((16, 64, 96))
+    eps = eps_noa(x, 1e-3)
+    xt = _t(x)
+    a = gpu.compress(xt, eps).cpu().numpy().tobytes()
+    for _ in range(3):
+        assert gpu.compress(xt, eps).cpu().numpy().tobytes() == a
+
+
+FULL = ["cfg4", "cfg2"]
+
+
+@pytest.mark.parametrize("name", FULL)
+def test_full_size_byte_parity(ref, gpu, name):
+    """BASELINE.json full sizes, same launch configuration as bench.py:
+    the whole stream is byte-compared with the oracle's."""
+    cfg = CONFIGS[name]
+    x = cfg.generate()
+    eps = eps_noa(x, cfg.rel)
+    xt = _t(x)
+    st_gpu = gpu.compress(xt, eps).cpu().numpy().tobytes()
+    st_ref = ref.compress(x, eps)
+    assert st_gpu == st_ref
+    y = gpu.decompress(_t(np.frombuffer(st_gpu, np.uint8).copy())).cpu().numpy()
+    assert ref.order_violations(x, y) == 0
+    assert ref.bound_violations(x, y, eps) == 0
+    s = ref.subbins(x, eps)
+    assert y.tobytes() == ref.reconstruct(x, eps, s).tobytes()
+
+
+def test_full_size_cfg3_certificate(ref, gpu):
+    """cfg3 (512^3): the GPU subbins satisfy the Bellman equation everywhere
+    (so they ARE the unique least fixpoint, O9), the decoded field equals
+    the oracle's O10 reconstruction bit for bit, and sampled chunks of the
+    stream equal the oracle's chunk encoder byte for byte."""
+    cfg = CONFIGS["cfg3"]
+    x = cfg.generate()
+    eps = eps_noa(x, cfg.rel)
+    xt = _t(x)
+    _, s = gpu.repair(xt, eps)
+    s = s.cpu().numpy().view(np.uint32)
+    assert ref.certify(x, eps, s) == 0
+    st = gpu.compress(xt, eps)
+    y = gpu.decompress(st).cpu().numpy()
+    assert y.tobytes() == ref.reconstruct(x, eps, s).tobytes()
+    assert ref.order_violations(x, y) == 0
+    assert ref.bound_violations(x, y, eps) == 0
+    stb = st.cpu().numpy().tobytes()
+    sizes = ref.chunk_sizes(stb)
+    offs = 64 + 8 * len(sizes) + np.concatenate([[0], np.cumsum(sizes.sum(axis=1))])
+    rng = np.random.default_rng(3)
+    for c in sorted({0, len(sizes) - 1, *rng.integers(0, len(sizes), 40).tolist()}):
+        b, u = ref.encode_chunk(x, eps, s, int(c))
+        o = int(offs[c])
+        assert stb[o:o + len(b)] == b and stb[o + len(b):o + len(b) + len(u)] == u
