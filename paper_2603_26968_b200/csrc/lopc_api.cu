@@ -373,10 +373,11 @@ int lopc_stream_info(const void* host_hdr, size_t n, int* ndims, uint64_t* dims3
 
 int lopc_compress_ex(const void* in, int ndims, const uint64_t* dims, int dtype, double eps, void* out,
                      size_t* out_bytes, void* workspace, size_t workspace_bytes, void* stream) {
-  if (!out_bytes || !out || (!in)) return LOPC_E_ARG;
+  if (!out_bytes) return LOPC_E_ARG;
   Shape sh;
   int rc = make_shape(ndims, dims, dtype, sh);
   if (rc) return rc;
+  if (!out || (!in && sh.n)) return LOPC_E_ARG;
   if ((rc = check_eps(eps))) return rc;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const bool host_in = !is_device_ptr(in), host_out = !is_device_ptr(out);
@@ -536,7 +537,8 @@ int lopc_repair_ex(const void* in, int ndims, const uint64_t* dims, int dtype, d
 
 int lopc_decompress_ex(const void* in, size_t in_bytes, void* out, size_t out_capacity, void* workspace,
                        size_t workspace_bytes, void* stream) {
-  if (!in || !out) return LOPC_E_ARG;
+  if (!in) return LOPC_E_ARG;
+  if (!out && out_capacity) return LOPC_E_ARG;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const bool host_in = !is_device_ptr(in), host_out = !is_device_ptr(out);
   const size_t cmax = in_bytes > kHdrBytes ? (in_bytes - kHdrBytes) / 16 + 1 : 1;
