@@ -234,7 +234,10 @@ def main():
             kern["encode"].append(sc["ms_encode"])
             kern["decode"].append(sd["ms_decode"])
             passes.append(sc["sweep_passes"])
-            tiles.append(sc["tiles_processed"])
+            tiles.append(sc["worklist_points"])
+            rep = {k: sc[k] for k in ("sweep_passes", "worklist_points", "inner_iters", "raised", "max_subbin",
+                                      "escapes", "n_tiles", "bin_bytes", "sub_bytes")}
+            rep["pass_items"] = [v for v in sc["pass_items"][1:] if v]
     torch.cuda.synchronize()
     lopc.set_timing(False)
     total_ms = sum(comp_ms) + sum(dec_ms)
@@ -284,8 +287,9 @@ def main():
     alg = {
         # read x, write flags + s
         "quant_repair": n * (k + F + 4),
-        # per processed tile point: read flags + s (write traffic not counted)
-        "sweep": statistics.median(tiles) * tiles_pts * (F + 4),
+        # dense pass: read flags, write s; sparse passes: per worklist point
+        # read flags + s (neighbour re-reads are served by L2, not counted)
+        "sweep": n * (F + 4) + statistics.median(tiles) * (F + 4),
         # read x + s, write the stream
         "encode": n * (k + 4) + nbytes_stream,
         # read the stream, write x^
@@ -316,7 +320,7 @@ def main():
         "decompress_GBps": raw * world * K / (dm / 1e3) / 1e9,
         "ratio": raw / nbytes_stream, "stream_bytes": nbytes_stream,
         "order_violations": violations, "bound_violations": bound_bad,
-        "sweep_passes": statistics.median(passes), "tiles_processed": statistics.median(tiles),
+        "repair": rep,
         "per_kernel": per_kernel,
         "roofline": {"kernel": f"k_{dom}", "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src},

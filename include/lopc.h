@@ -99,9 +99,9 @@ typedef struct {
   uint64_t n_elems;
   uint64_t n_chunks;
   uint64_t n_tiles;
-  uint64_t sweep_passes;      /* global passes of k_sweep after k_quant_repair */
-  uint64_t tiles_processed;   /* sum of active tiles over those passes */
-  uint64_t inner_iters;       /* sum of tile-local relaxation iterations */
+  uint64_t sweep_passes;      /* k_sweep passes: 1 dense tile pass + sparse point-worklist passes */
+  uint64_t worklist_points;   /* sum of worklist points over the sparse passes */
+  uint64_t inner_iters;       /* sum of tile-local relaxation rounds in the dense pass */
   uint64_t escapes;
   uint64_t bin_bytes;
   uint64_t sub_bytes;
@@ -109,12 +109,14 @@ typedef struct {
   uint32_t max_subbin;
   uint32_t timing_valid;      /* 1 if the ms_* fields were measured (lopc_set_timing) */
   float ms_h2d;               /* host->device staging */
-  float ms_quant_repair;      /* k_quant_repair */
+  float ms_quant_repair;      /* k_quant_flags (a1 + a2) */
   float ms_sweep;             /* k_sweep */
   float ms_encode;            /* k_encode */
   float ms_decode;            /* k_decode */
   float ms_d2h;               /* device->host staging */
   float ms_total;             /* whole call on the stream */
+  uint64_t raised;            /* subbins raised above 0 (dense pass) or raised again (sparse passes) */
+  uint32_t pass_items[16];    /* [1]: tiles of the dense pass; [q>1]: worklist points of pass q */
 } lopc_stats;
 
 int lopc_last_stats(lopc_stats* out);

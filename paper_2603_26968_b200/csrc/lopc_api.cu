@@ -1,6 +1,6 @@
 // lopc_api.cu — host orchestration behind include/lopc.h (liblopc.so).
 //
-// compress:   [H2D stage] -> k_quant_repair -> k_sweep (cooperative, device-
+// compress:   [H2D stage] -> k_quant_flags -> k_sweep (cooperative, device-
 //             side termination) -> k_encode (look-back placement, header) ->
 //             one D2H read of the status block -> [D2H stage]
 // decompress: [H2D stage] -> k_decode (persistent, header validated on the
@@ -75,7 +75,8 @@ int check_eps(double eps) {
 inline size_t al(size_t v) { return (v + 255) & ~size_t(255); }
 
 struct CLayout {
-  size_t ctr, stamp, state, zero_end, lists, flags, s, stage_in, stage_out, total;
+  size_t ctr, bitmap, state, zero_end, plist, flags, s, stage_in, stage_out, total;
+  uint64_t bmw, nseg;
   int ntz, nty, ntx;
   uint64_t ntiles;
 };
@@ -95,15 +96,17 @@ CLayout compress_layout(const Shape& s, bool host_in, bool host_out) {
   size_t o = 0;
   L.ctr = o;
   o += al(sizeof(Counters));
-  L.stamp = o;
-  o += al(4 * L.ntiles);
+  L.bmw = (s.n + 31) / 32;
+  L.bitmap = o;
+  o += al(2 * 4 * L.bmw);
   L.state = o;
   o += al(8 * s.C);
   L.zero_end = o;
-  L.lists = o;
-  o += al(3 * 4 * L.ntiles);
+  L.plist = o;
+  o += al(2 * (s.n < (1ull << 31) - (1ull << 24) ? 4 : 8) * s.n);
+  L.nseg = (s.d2 + 31) / 32;
   L.flags = o;
-  o += al((s.ndims == 3 ? 2 : 1) * s.n);
+  o += al(4ull * s.d0 * s.d1 * L.nseg * (s.ndims == 3 ? Geo<3>::SW : Geo<2>::SW));
   L.s = o;
   o += al(4 * s.n);
   L.stage_in = o;
@@ -125,7 +128,7 @@ bool is_device_ptr(const void* p) {
 
 struct DevInfo {
   int dev = -1, sms = 0;
-  int occ_sweep2 = 0, occ_sweep3 = 0, occ_decode = 0;
+  int occ_sweep2 = 0, occ_sweep3 = 0, occ_sweep2w = 0, occ_sweep3w = 0, occ_decode = 0;
   bool attrs = false;
 };
 DevInfo g_dev;
@@ -141,16 +144,17 @@ int dev_info(DevInfo*& out) {
     CK(cudaFuncSetAttribute(k_encode<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     CK(cudaFuncSetAttribute(k_encode<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     CK(cudaFuncSetAttribute(k_decode, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    CK(cudaFuncSetAttribute(k_quant_repair<float, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)quant_repair_smem<float, 3>()));
-    CK(cudaFuncSetAttribute(k_quant_repair<float, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)quant_repair_smem<float, 2>()));
-    CK(cudaFuncSetAttribute(k_quant_repair<double, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)quant_repair_smem<double, 3>()));
-    CK(cudaFuncSetAttribute(k_quant_repair<double, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)quant_repair_smem<double, 2>()));
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_dev.occ_sweep2, k_sweep<2>, kRepairThreads, 0));
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_dev.occ_sweep3, k_sweep<3>, kRepairThreads, 0));
+#define QRA(TT, ND)                                                                                      \
+  CK(cudaFuncSetAttribute(k_quant_flags<TT, ND, int32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,     \
+                          (int)quant_flags_smem<TT, ND>()));                                               \
+  CK(cudaFuncSetAttribute(k_quant_flags<TT, ND, int64_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,     \
+                          (int)quant_flags_smem<TT, ND>()));
+    QRA(float, 3) QRA(float, 2) QRA(double, 3) QRA(double, 2)
+#undef QRA
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_dev.occ_sweep2, k_sweep<2, int32_t>, kSweepThreads, 0));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_dev.occ_sweep3, k_sweep<3, int32_t>, kSweepThreads, 0));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_dev.occ_sweep2w, k_sweep<2, int64_t>, kSweepThreads, 0));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_dev.occ_sweep3w, k_sweep<3, int64_t>, kSweepThreads, 0));
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_dev.occ_decode, k_decode, kCodecThreads, smem));
     g_dev.attrs = true;
   }
@@ -227,10 +231,13 @@ int run_repair(const Shape& sh, const void* x, double eps, uint8_t* ws, const CL
   if (rc) return rc;
   RepairArgs ra{};
   ra.x = x;
-  ra.flags = ws + L.flags;
+  ra.flags = reinterpret_cast<uint32_t*>(ws + L.flags);
+  ra.nseg = (int64_t)L.nseg;
   ra.s = reinterpret_cast<uint32_t*>(ws + L.s);
-  ra.stamp = reinterpret_cast<uint32_t*>(ws + L.stamp);
-  ra.lists = reinterpret_cast<uint32_t*>(ws + L.lists);
+  ra.plist = ws + L.plist;
+  ra.bitmap = reinterpret_cast<uint32_t*>(ws + L.bitmap);
+  ra.cap = sh.n;
+  ra.bmw = L.bmw;
   ra.ctr = reinterpret_cast<Counters*>(ws + L.ctr);
   ra.eps = eps;
   ra.inv = 1.0 / eps;
@@ -241,31 +248,39 @@ int run_repair(const Shape& sh, const void* x, double eps, uint8_t* ws, const CL
   ra.nty = L.nty;
   ra.ntx = L.ntx;
   ra.ntiles = (int64_t)L.ntiles;
-  ra.max_inner = 64;
   ra.max_passes = 1 << 20;
-  const unsigned nt = (unsigned)L.ntiles;
-  if (sh.dtype == LOPC_F32) {
-    if (sh.ndims == 3)
-      k_quant_repair<float, 3><<<nt, kRepairThreads, quant_repair_smem<float, 3>(), st>>>(ra);
-    else
-      k_quant_repair<float, 2><<<nt, kRepairThreads, quant_repair_smem<float, 2>(), st>>>(ra);
-  } else {
-    if (sh.ndims == 3)
-      k_quant_repair<double, 3><<<nt, kRepairThreads, quant_repair_smem<double, 3>(), st>>>(ra);
-    else
-      k_quant_repair<double, 2><<<nt, kRepairThreads, quant_repair_smem<double, 2>(), st>>>(ra);
-  }
-  CK(cudaGetLastError());
-  tm.mark();
-  int occ = sh.ndims == 3 ? di->occ_sweep3 : di->occ_sweep2;
+  const dim3 tgrid((unsigned)L.ntx, (unsigned)L.nty, (unsigned)L.ntz);
+  const bool i32 = sh.n < (1ull << 31) - (1ull << 24);
+  int occ = sh.ndims == 3 ? (i32 ? di->occ_sweep3 : di->occ_sweep3w) : (i32 ? di->occ_sweep2 : di->occ_sweep2w);
   uint64_t grid = (uint64_t)occ * di->sms;
   if (grid > L.ntiles) grid = L.ntiles;
   if (grid < 1) grid = 1;
   void* kargs[] = {&ra};
-  if (sh.ndims == 3)
-    CK(cudaLaunchCooperativeKernel((void*)k_sweep<3>, dim3((unsigned)grid), dim3(kRepairThreads), kargs, 0, st));
-  else
-    CK(cudaLaunchCooperativeKernel((void*)k_sweep<2>, dim3((unsigned)grid), dim3(kRepairThreads), kargs, 0, st));
+#define QR(TT, ND, IX) k_quant_flags<TT, ND, IX><<<tgrid, kRepairThreads, quant_flags_smem<TT, ND>(), st>>>(ra)
+#define SW(ND, IX)                                                                                               \
+  CK(cudaLaunchCooperativeKernel((void*)k_sweep<ND, IX>, dim3((unsigned)grid), dim3(kSweepThreads), kargs, 0, st))
+  if (i32) {
+    if (sh.dtype == LOPC_F32) {
+      if (sh.ndims == 3) QR(float, 3, int32_t); else QR(float, 2, int32_t);
+    } else {
+      if (sh.ndims == 3) QR(double, 3, int32_t); else QR(double, 2, int32_t);
+    }
+  } else {
+    if (sh.dtype == LOPC_F32) {
+      if (sh.ndims == 3) QR(float, 3, int64_t); else QR(float, 2, int64_t);
+    } else {
+      if (sh.ndims == 3) QR(double, 3, int64_t); else QR(double, 2, int64_t);
+    }
+  }
+  CK(cudaGetLastError());
+  tm.mark();
+  if (i32) {
+    if (sh.ndims == 3) SW(3, int32_t); else SW(2, int32_t);
+  } else {
+    if (sh.ndims == 3) SW(3, int64_t); else SW(2, int64_t);
+  }
+#undef QR
+#undef SW
   tm.mark();
   (void)hc;
   return LOPC_OK;
@@ -403,6 +418,7 @@ int lopc_compress_ex(const void* in, int ndims, const uint64_t* dims, int dtype,
     return LOPC_OK;
   }
   const CLayout L = compress_layout(sh, host_in, host_out);
+  if (L.nty > 65535 || L.ntz > 65535) return LOPC_E_SHAPE;  // tile launch grid limit
   if (!workspace || workspace_bytes < L.total) return LOPC_E_NOSPACE;
   uint8_t* ws = static_cast<uint8_t*>(workspace);
   g_stats.n_tiles = L.ntiles;
@@ -434,6 +450,7 @@ int lopc_compress_ex(const void* in, int ndims, const uint64_t* dims, int dtype,
   ea.n = sh.n;
   ea.C = (uint32_t)sh.C;
   ea.ndims = sh.ndims;
+  ea.vec = ((uintptr_t)x % 16 == 0) && ((uintptr_t)ea.s % 16 == 0);
   ea.d0 = sh.d0;
   ea.d1 = sh.d1;
   ea.d2 = sh.d2;
@@ -448,15 +465,17 @@ int lopc_compress_ex(const void* in, int ndims, const uint64_t* dims, int dtype,
   CK(cudaStreamSynchronize(st));
   const uint64_t total = hc->total_bytes;
   g_stats.sweep_passes = hc->passes;
-  g_stats.tiles_processed = hc->tiles_processed;
+  g_stats.worklist_points = hc->worklist_points;
   g_stats.inner_iters = hc->inner_iters;
   g_stats.escapes = hc->escapes;
   g_stats.bin_bytes = hc->bin_bytes;
   g_stats.sub_bytes = hc->sub_bytes;
   g_stats.total_bytes = total;
   g_stats.max_subbin = hc->max_s;
+  g_stats.raised = hc->raised;
+  for (int i = 0; i < 16; ++i) g_stats.pass_items[i] = hc->pass_items[i];
   uint32_t err = hc->err;
-  if (hc->list_count[(hc->passes + 1) % 3] != 0 && hc->passes >= (1ull << 20)) err |= kErrPassCap;
+  if (hc->passes >= (unsigned long long)(1 << 20) && hc->list_count[(hc->passes + 1) % 3] != 0) err |= kErrPassCap;
   if ((rc = map_err(err & ~kErrNoSpace))) return rc;
   if (total > cap) {
     *out_bytes = total;
@@ -506,6 +525,7 @@ int lopc_repair_ex(const void* in, int ndims, const uint64_t* dims, int dtype, d
   if (!is_device_ptr(in)) return LOPC_E_ARG;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const CLayout L = compress_layout(sh, false, false);
+  if (L.nty > 65535 || L.ntz > 65535) return LOPC_E_SHAPE;
   if (!workspace || workspace_bytes < L.total) return LOPC_E_NOSPACE;
   uint8_t* ws = static_cast<uint8_t*>(workspace);
   Counters* hc;
@@ -515,13 +535,12 @@ int lopc_repair_ex(const void* in, int ndims, const uint64_t* dims, int dtype, d
   if ((rc = run_repair(sh, in, eps, ws, L, st, tm, hc))) return rc;
   if (subbins_out) CK(cudaMemcpyAsync(subbins_out, ws + L.s, 4 * sh.n, cudaMemcpyDeviceToDevice, st));
   if (flags_out) {
-    if (sh.ndims == 3) {
-      CK(cudaMemcpyAsync(flags_out, ws + L.flags, 2 * sh.n, cudaMemcpyDeviceToDevice, st));
-    } else {
-      // widen u8 -> u16 with a strided 2D copy into the low bytes
-      CK(cudaMemsetAsync(flags_out, 0, 2 * sh.n, st));
-      CK(cudaMemcpy2DAsync(flags_out, 2, ws + L.flags, 1, 1, sh.n, cudaMemcpyDeviceToDevice, st));
-    }
+    const uint32_t* fw = reinterpret_cast<const uint32_t*>(ws + L.flags);
+    if (sh.ndims == 3)
+      k_unpack_flags<3><<<1024, 256, 0, st>>>(fw, flags_out, sh.d0, sh.d1, sh.d2, (int64_t)L.nseg);
+    else
+      k_unpack_flags<2><<<1024, 256, 0, st>>>(fw, flags_out, sh.d0, sh.d1, sh.d2, (int64_t)L.nseg);
+    CK(cudaGetLastError());
   }
   CK(cudaMemcpyAsync(hc, ws + L.ctr, sizeof(Counters), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
@@ -529,9 +548,11 @@ int lopc_repair_ex(const void* in, int ndims, const uint64_t* dims, int dtype, d
   g_stats.n_elems = sh.n;
   g_stats.n_tiles = L.ntiles;
   g_stats.sweep_passes = hc->passes;
-  g_stats.tiles_processed = hc->tiles_processed;
+  g_stats.worklist_points = hc->worklist_points;
   g_stats.inner_iters = hc->inner_iters;
   g_stats.max_subbin = hc->max_s;
+  g_stats.raised = hc->raised;
+  for (int i = 0; i < 16; ++i) g_stats.pass_items[i] = hc->pass_items[i];
   return map_err(hc->err);
 }
 

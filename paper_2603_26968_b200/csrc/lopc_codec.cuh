@@ -366,6 +366,7 @@ struct EncodeArgs {
   uint64_t n;
   uint32_t C;
   int ndims;
+  int vec;  // x and s are 16-byte aligned: vector loads allowed
   uint64_t d0, d1, d2;
 };
 
@@ -383,25 +384,36 @@ struct CodecSmem {
 
 constexpr uint64_t kFlagAgg = 1ull << 62, kFlagIncl = 2ull << 62, kValMask = (1ull << 62) - 1;
 
-// decoupled look-back (one thread): publish the aggregate, sum predecessors.
-__device__ __forceinline__ uint64_t lookback(uint64_t* state, uint32_t c, uint64_t agg) {
+// Decoupled look-back, one warp: publish this chunk's aggregate, then sum the
+// predecessors 32 at a time (lane i looks at chunk c-1-i) until the nearest
+// inclusive prefix is found; publish the inclusive prefix.  Returns the
+// exclusive prefix in every lane.  Forward progress: chunk ids come from a
+// ticket in scheduling order, so every predecessor is already running.
+__device__ __forceinline__ uint64_t lookback_warp(uint64_t* state, uint32_t c, uint64_t agg) {
+  const int lane = threadIdx.x & 31;
   if (c == 0) {
-    st_release_u64(&state[0], kFlagIncl | agg);
+    if (lane == 0) st_release_u64(&state[0], kFlagIncl | agg);
     return 0;
   }
-  st_release_u64(&state[c], kFlagAgg | agg);
+  if (lane == 0) st_release_u64(&state[c], kFlagAgg | agg);
   uint64_t excl = 0;
-  int64_t i = (int64_t)c - 1;
+  int64_t base = (int64_t)c - 1;
   for (;;) {
-    uint64_t v;
-    do {
-      v = ld_acquire_u64(&state[i]);
-    } while ((v >> 62) == 0);
-    excl += v & kValMask;
-    if ((v >> 62) == 2) break;
-    --i;
+    const int64_t i = base - lane;
+    const uint64_t v = i >= 0 ? ld_acquire_u64(&state[i]) : kFlagIncl;
+    const uint32_t incl = __ballot_sync(0xffffffffu, (v >> 62) == 2);
+    const uint32_t none = __ballot_sync(0xffffffffu, (v >> 62) == 0);
+    const int first = incl ? __ffs(incl) - 1 : 31;
+    const uint32_t need = first == 31 ? 0xffffffffu : ((2u << first) - 1u);
+    if (none & need) continue;  // a predecessor has not published yet
+    uint64_t part = lane <= first ? (v & kValMask) : 0ull;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+    excl += part;
+    if (incl) break;
+    base -= 32;
   }
-  st_release_u64(&state[c], kFlagIncl | (excl + agg));
+  if (lane == 0) st_release_u64(&state[c], kFlagIncl | (excl + agg));
   return excl;
 }
 
@@ -430,31 +442,57 @@ __global__ void __launch_bounds__(kCodecThreads, 2) k_encode(EncodeArgs a) {
   const uint32_t* S = a.s + e0;
 
   // --- a1 + a4: re-quantize, words, bound self-check ---------------------
+  // each thread owns PER/4 runs of 4 consecutive words, loaded as 16-byte vectors
   uint32_t esc = 0, bad = 0;
 #pragma unroll
-  for (int v = 0; v < PER; ++v) {
-    const int i = v * kCodecThreads + tid;  // coalesced
-    U bw = 0, sw = 0;
-    if ((uint32_t)i < cnt) {
-      T x = X[i];
-      uint32_t s = S[i];
-      I b;
-      if (quantize<T>(x, a.eps, a.inv, b)) {
-        bw = (U)b;
-        sw = (U)s;
-        if (s != 0) {
-          // x^ = value with key(lo(b)) + s must not exceed x (a4)
-          T lo = lo_t<T>((int64_t)b, a.eps);
-          if ((int64_t)key_of((U)as_bits(lo)) + (int64_t)s > (int64_t)key_of((U)as_bits(x))) bad = 1;
-        }
+  for (int v = 0; v < PER / 4; ++v) {
+    const int i0 = 4 * (v * kCodecThreads + tid);
+    T xs[4];
+    uint32_t ss[4];
+    if (a.vec && (uint32_t)i0 + 3 < cnt) {
+      if constexpr (sizeof(T) == 4) {
+        const float4 xv = __ldg(reinterpret_cast<const float4*>(X + i0));
+        xs[0] = xv.x, xs[1] = xv.y, xs[2] = xv.z, xs[3] = xv.w;
       } else {
-        bw = VT<T>::kSentinel;
-        sw = (U)as_bits(x);
-        ++esc;
+        const double2 x0 = __ldg(reinterpret_cast<const double2*>(X + i0));
+        const double2 x1 = __ldg(reinterpret_cast<const double2*>(X + i0 + 2));
+        xs[0] = x0.x, xs[1] = x0.y, xs[2] = x1.x, xs[3] = x1.y;
+      }
+      const uint4 sv = __ldg(reinterpret_cast<const uint4*>(S + i0));
+      ss[0] = sv.x, ss[1] = sv.y, ss[2] = sv.z, ss[3] = sv.w;
+    } else {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const bool in = (uint32_t)(i0 + q) < cnt;
+        xs[q] = in ? X[i0 + q] : (T)0;
+        ss[q] = in ? S[i0 + q] : 0u;
       }
     }
-    WB[swz(i)] = bw;
-    WS[swz(i)] = sw;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int i = i0 + q;
+      U bw = 0, sw = 0;
+      if ((uint32_t)i < cnt) {
+        const T x = xs[q];
+        const uint32_t sq = ss[q];
+        I b;
+        if (quantize<T>(x, a.eps, a.inv, b)) {
+          bw = (U)b;
+          sw = (U)sq;
+          if (sq != 0) {
+            // x^ = value with key(lo(b)) + s must not exceed x (a4)
+            const T lo = lo_t<T>((int64_t)b, a.eps);
+            if ((int64_t)key_of((U)as_bits(lo)) + (int64_t)sq > (int64_t)key_of((U)as_bits(x))) bad = 1;
+          }
+        } else {
+          bw = VT<T>::kSentinel;
+          sw = (U)as_bits(x);
+          ++esc;
+        }
+      }
+      WB[swz(i)] = bw;
+      WS[swz(i)] = sw;
+    }
   }
   if (bad) atomicOr(&a.ctr->err, kErrBound);
   esc = __reduce_add_sync(0xffffffffu, esc);
@@ -494,9 +532,9 @@ __global__ void __launch_bounds__(kCodecThreads, 2) k_encode(EncodeArgs a) {
   }
 
   // --- a7: placement by decoupled look-back -----------------------------------
-  if (tid == 0) {
-    uint64_t excl = lookback(a.state, c, (uint64_t)bsize + ssize);
-    sm.misc64[0] = excl;
+  if (tid < 32) {
+    const uint64_t excl = lookback_warp(a.state, c, (uint64_t)bsize + ssize);
+    if (tid == 0) sm.misc64[0] = excl;
   }
   __syncthreads();
   const uint64_t base = (uint64_t)kHdrBytes + 8ull * a.C + sm.misc64[0];
@@ -751,22 +789,26 @@ __global__ void __launch_bounds__(kCodecThreads, 2) k_decode(DecodeArgs a) {
   }
   const uint32_t* tab = reinterpret_cast<const uint32_t*>(a.in + kHdrBytes);
   for (;;) {
-    if (tid == 0) {
-      uint32_t c = atomicAdd(&a.ctr->ticket, 1u);
-      sm.misc[0] = c;
+    if (tid < 32) {
+      uint32_t c = 0;
+      if (tid == 0) c = atomicAdd(&a.ctr->ticket, 1u);
+      c = __shfl_sync(0xffffffffu, c, 0);
+      if (tid == 0) sm.misc[0] = c;
       if (c < h.C) {
-        uint32_t bs = tab[2 * c], ss = tab[2 * c + 1];
+        const uint32_t bs = tab[2 * c], ss = tab[2 * c + 1];
         bool ok = bs >= 4 && bs <= kChunkBytes && (bs & 3u) == 0 && ss >= 4 && ss <= kChunkBytes && (ss & 3u) == 0;
-        uint64_t agg = ok ? (uint64_t)bs + ss : (1ull << 40);  // poison keeps later offsets out of range
-        uint64_t excl = lookback(a.state, c, agg);
-        uint64_t off = (uint64_t)kHdrBytes + 8ull * h.C + excl;
+        const uint64_t agg = ok ? (uint64_t)bs + ss : (1ull << 40);  // poison keeps later offsets out of range
+        const uint64_t excl = lookback_warp(a.state, c, agg);
+        const uint64_t off = (uint64_t)kHdrBytes + 8ull * h.C + excl;
         if (!ok || off + bs + ss > a.in_bytes) ok = false;
         if (c == h.C - 1 && off + bs + ss != a.in_bytes) ok = false;
-        if (!ok) atomicOr(&a.ctr->err, kErrCorrupt);
-        sm.misc[1] = ok;
-        sm.misc[2] = bs;
-        sm.misc[3] = ss;
-        sm.misc64[0] = off;
+        if (tid == 0) {
+          if (!ok) atomicOr(&a.ctr->err, kErrCorrupt);
+          sm.misc[1] = ok;
+          sm.misc[2] = bs;
+          sm.misc[3] = ss;
+          sm.misc64[0] = off;
+        }
       }
     }
     __syncthreads();

@@ -7,25 +7,39 @@
 // any monotone relaxation schedule reaches it (reading G14).  The schedule
 // here is B200-shaped, not the paper's point worklist:
 //
-//   k_quant_repair  one CTA per 3D tile (8x8x32, 2D: 32x64) with a one-cell
-//                   halo in shared memory: exact bins of tile+halo, flags of
-//                   the tile (u16 in 3D / u8 in 2D), relaxation inside the
-//                   tile to local convergence with the halo held at 0 (a lower
-//                   bound), write flags + s.  Tiles whose boundary subbins are
-//                   > 0 and feed a neighbour tile enlist that tile.
-//   k_sweep         one persistent cooperative kernel: pass q processes the
-//                   active-tile list q (halo s re-read from global), relaxes
-//                   each tile to local convergence, writes raised subbins and
-//                   enlists the neighbour tiles its raised boundary points
-//                   feed; grid-wide barrier; stop when a list is empty.  No
-//                   host round trip per sweep.
+//   k_quant_flags   one CTA per 2048-point tile (3D 8x8x32, 2D 64x32) with a
+//                   one-cell halo of value keys in shared memory.  Only the
+//                   tile's own points are quantized: with K_lo(p) =
+//                   key(lo(b_p)), a neighbour n is a same-bin predecessor of p
+//                   iff K_lo(p) <= key(n) < key(p) (+e slots; <= for -e slots,
+//                   the SoS tie rule G4), because bins are key intervals.
+//                   Flags are stored as bit planes: for every 32-point x-row
+//                   segment, word j holds star slot j of its 32 points (one
+//                   warp ballot per slot).
+//   k_sweep         one persistent cooperative kernel.
+//     pass 1        dense, one warp per tile, bit-parallel: the level sets
+//                   Lev_L = {p : s(p) >= L} of the tile-local fixpoint (halo
+//                   held at 0) satisfy
+//                     Lev_L = mu X. OR_{+e j} F_j & Lev_{L-1}(p + e_j)
+//                                 | OR_{-e j} F_j & X(p - e_j),
+//                   computed 32 points per word: the -e closure is a Jacobi
+//                   loop over rows with a carry-lookahead fill along x.  s is
+//                   the number of non-empty levels.  A point with s > 0 on
+//                   the tile border enqueues the out-of-tile points it feeds.
+//     passes >= 2   sparse, point-level: the paper's own worklist schedule
+//                   (Alg. 2 with the dual worklists of P:220, atomicMax P:218)
+//                   on the remaining tail; a raised point enqueues its
+//                   successors.  Grid-wide barrier between passes; stop when
+//                   a worklist is empty.  No host round trip per pass.
 //
 // Every value ever written is <= the least fixpoint (lower bounds relaxed by
-// monotone max), and on exit every tile was last processed with its current
-// halo and is locally stable, so the Bellman equation holds everywhere: the
-// result is the least fixpoint, independent of scheduling.
+// monotone max), and when the worklist empties every point satisfies the
+// Bellman equation, so the result is the least fixpoint, independent of
+// scheduling.
 #pragma once
 #include <cooperative_groups.h>
+
+#include <type_traits>
 
 #include "lopc_device.cuh"
 
@@ -37,56 +51,67 @@ template <>
 struct Geo<3> {
   static constexpr int TZ = 8, TY = 8, TX = 32;
   static constexpr int HZ = TZ + 2, HY = TY + 2, HX = TX + 2;
-  static constexpr int D = 7;  // +e offsets (G2)
-  using Flag = uint16_t;
+  static constexpr int ZH = 1;
+  static constexpr int D = 7;   // +e offsets (G2)
+  static constexpr int SW = 16; // words per 32-point flag segment (14 used)
 };
 template <>
 struct Geo<2> {
-  static constexpr int TZ = 1, TY = 32, TX = 64;
+  static constexpr int TZ = 1, TY = 64, TX = 32;
   static constexpr int HZ = 1, HY = TY + 2, HX = TX + 2;
+  static constexpr int ZH = 0;
   static constexpr int D = 3;
-  using Flag = uint8_t;
+  static constexpr int SW = 8;  // 6 used
 };
 
 constexpr int kRepairThreads = 512;
+constexpr int kSweepThreads = 256;
+constexpr int kSweepWarps = kSweepThreads / 32;
+constexpr int kPassHist = 16;
+constexpr int kLevelPlanes = 8;  // dense-pass levels per tile before handing over to the worklist
+constexpr int kMaxLevel = (1 << kLevelPlanes) - 1;
 
-// Star slot j (G2): j < D is +e_j, j >= D is -e_{j-D}.  3D order (dz,dy,dx):
-// (0,0,1) (0,1,0) (0,1,1) (1,0,0) (1,0,1) (1,1,0) (1,1,1); 2D (dy,dx):
-// (0,1) (1,0) (1,1).
+// Star slot j (G2): j < D is +e, j >= D is -e, with e = (j mod D) + 1 read
+// as bits (dz, dy, dx) in 3D and (dy, dx) in 2D: 3D order (0,0,1) (0,1,0)
+// (0,1,1) (1,0,0) (1,0,1) (1,1,0) (1,1,1); 2D (0,1) (1,0) (1,1).
 template <int NDIM>
-__host__ __device__ constexpr int slot_dz(int j) {
-  return NDIM == 2 ? 0 : (j % 7 >= 3 ? (j < 7 ? 1 : -1) : 0);
+__host__ __device__ __forceinline__ constexpr int slot_dz(int j) {
+  return NDIM == 2 ? 0 : (j < Geo<NDIM>::D ? 1 : -1) * ((((j % Geo<NDIM>::D) + 1) >> 2) & 1);
 }
 template <int NDIM>
-__host__ __device__ constexpr int slot_dy(int j) {
-  return NDIM == 2 ? ((j % 3) >= 1 ? (j < 3 ? 1 : -1) : 0)
-                   : (((j % 7) == 1 || (j % 7) == 2 || (j % 7) == 5 || (j % 7) == 6) ? (j < 7 ? 1 : -1) : 0);
+__host__ __device__ __forceinline__ constexpr int slot_dy(int j) {
+  return (j < Geo<NDIM>::D ? 1 : -1) * ((((j % Geo<NDIM>::D) + 1) >> 1) & 1);
 }
 template <int NDIM>
-__host__ __device__ constexpr int slot_dx(int j) {
-  return NDIM == 2 ? ((j % 3) != 1 ? (j < 3 ? 1 : -1) : 0)
-                   : (((j % 7) == 0 || (j % 7) == 2 || (j % 7) == 4 || (j % 7) == 6) ? (j < 7 ? 1 : -1) : 0);
+__host__ __device__ __forceinline__ constexpr int slot_dx(int j) {
+  return (j < Geo<NDIM>::D ? 1 : -1) * (((j % Geo<NDIM>::D) + 1) & 1);
 }
 template <int NDIM>
-__host__ __device__ constexpr int slot_hoff(int j) {
+__host__ __device__ __forceinline__ constexpr int slot_hoff(int j) {
   using G = Geo<NDIM>;
   return slot_dz<NDIM>(j) * G::HY * G::HX + slot_dy<NDIM>(j) * G::HX + slot_dx<NDIM>(j);
 }
+template <int NDIM>
+__host__ __device__ __forceinline__ constexpr int slot_opp(int j) {
+  return j < Geo<NDIM>::D ? j + Geo<NDIM>::D : j - Geo<NDIM>::D;
+}
 
 struct Counters {
-  uint32_t list_count[3];
+  uint32_t pad0[3];
   uint32_t ticket;
-  uint32_t err;  // bit 0 bound self-check, 1 corrupt, 2 nospace, 3 subbin overflow, 4 pass cap
+  uint32_t err;  // kErr* bits
   uint32_t max_s;
   uint32_t pad[2];
   unsigned long long escapes;
   unsigned long long total_bytes;
   unsigned long long passes;
-  unsigned long long tiles_processed;
+  unsigned long long worklist_points;
   unsigned long long bin_bytes;
   unsigned long long sub_bytes;
   unsigned long long inner_iters;
-  unsigned long long pad2;
+  unsigned long long raised;
+  unsigned long long list_count[3];  // point worklists (rotating)
+  uint32_t pass_items[kPassHist];    // [1] tiles of the dense pass, [q>1] worklist points of pass q
 };
 
 enum : uint32_t {
@@ -100,324 +125,468 @@ enum : uint32_t {
 
 struct RepairArgs {
   const void* x;
-  void* flags;
+  uint32_t* flags;    // bit-plane flags: segment (z, y, xs) at ((z*d1 + y)*nseg + xs)*SW
   uint32_t* s;
-  uint32_t* stamp;   // per tile: last pass it was enlisted for
-  uint32_t* lists;   // 3 x ntiles
+  void* plist;        // 2 x cap point indices (Idx-sized), worklists of passes >= 2
+  uint32_t* bitmap;   // 2 x bmw words: per-point "already enqueued" bits, self-clearing
+  uint64_t cap;       // entries per worklist (= N)
+  uint64_t bmw;       // words per bitmap
   Counters* ctr;
   double eps, inv;
   int64_t d0, d1, d2;  // z, y, x extents (2D: d0 = 1)
+  int64_t nseg;        // 32-point segments per x-row
   int ntz, nty, ntx;
   int64_t ntiles;
-  int max_inner;
   int max_passes;
 };
 
-__device__ __forceinline__ void enlist(const RepairArgs& a, uint32_t tile, uint32_t q) {
-  uint32_t old = atomicMax(&a.stamp[tile], q);
-  if (old < q) {
-    uint32_t slot = atomicAdd(&a.ctr->list_count[q % 3], 1u);
-    a.lists[(size_t)(q % 3) * a.ntiles + slot] = tile;
+// Enqueue point q for pass `pass` (dedup by the pass's bitmap).
+template <typename Idx>
+__device__ __forceinline__ void enqueue(const RepairArgs& a, Idx q, int pass) {
+  using UIdx = typename std::make_unsigned<Idx>::type;
+  const uint32_t bit = 1u << ((uint32_t)q & 31u);
+  const uint32_t old = atomicOr(&a.bitmap[(size_t)(pass & 1) * a.bmw + ((UIdx)q >> 5)], bit);
+  if (!(old & bit)) {
+    const unsigned long long slot = atomicAdd(&a.ctr->list_count[pass % 3], 1ull);
+    static_cast<UIdx*>(a.plist)[(size_t)(pass & 1) * a.cap + slot] = (UIdx)q;
   }
 }
 
-// Enlist the neighbour tiles recorded as bits (dz+1)*9 + (dy+1)*3 + (dx+1).
-__device__ __forceinline__ void enlist_dirs(const RepairArgs& a, uint32_t dirs, int tz, int ty, int tx, uint32_t q) {
-  int t = threadIdx.x;
-  if (t < 27 && ((dirs >> t) & 1u)) {
-    int nz = tz + t / 9 - 1, ny = ty + (t / 3) % 3 - 1, nx = tx + t % 3 - 1;
-    if (nz >= 0 && ny >= 0 && nx >= 0 && nz < a.ntz && ny < a.nty && nx < a.ntx)
-      enlist(a, (uint32_t)(((int64_t)nz * a.nty + ny) * a.ntx + nx), q);
-  }
-}
-
+// Rows of the halo box handled per warp, and elements per lane per row.
 template <int NDIM>
-__device__ __forceinline__ int dir_of_halo(int hz, int hy, int hx) {
-  using G = Geo<NDIM>;
-  int dz = NDIM == 2 ? 0 : (hz == 0 ? -1 : (hz == G::HZ - 1 ? 1 : 0));
-  int dy = hy == 0 ? -1 : (hy == G::HY - 1 ? 1 : 0);
-  int dx = hx == 0 ? -1 : (hx == G::HX - 1 ? 1 : 0);
-  return (dz + 1) * 9 + (dy + 1) * 3 + (dx + 1);
+struct HaloRows {
+  static constexpr int R = Geo<NDIM>::HZ * Geo<NDIM>::HY;
+  static constexpr int RPW = (R + kRepairThreads / 32 - 1) / (kRepairThreads / 32);
+  static constexpr int EPL = (Geo<NDIM>::HX + 31) / 32;
+};
+
+template <typename T>
+__device__ __forceinline__ T value_of_key(typename VT<T>::I k);
+template <>
+__device__ __forceinline__ float value_of_key<float>(int32_t k) {
+  return __uint_as_float(bits_of_key32(k));
+}
+template <>
+__device__ __forceinline__ double value_of_key<double>(int64_t k) {
+  return __longlong_as_double((long long)bits_of_key64(k));
 }
 
-// Relax the tile's points to local convergence in shared memory.  Each thread
-// owns PPT points (flags in registers).  Returns the number of inner
-// iterations; *capped set if the cap was hit while still changing.
-template <int NDIM, int PPT>
-__device__ __forceinline__ int relax_tile(uint32_t* ss, const uint32_t (&f)[PPT], const int (&h)[PPT], int max_inner,
-                                          bool* capped) {
-  constexpr int D = Geo<NDIM>::D;
-  int it = 0;
-  for (;;) {
-    int changed = 0;
+// Load a (HZ x HY x HX) halo box of words starting at grid coordinate
+// (z0 - ZH, y0 - 1, x0 - 1) into registers, one warp per row; every load is
+// issued before any use.  Out-of-grid elements read as `fill`.
+template <int NDIM, typename W, typename Idx>
+struct HaloLoad {
+  using HR = HaloRows<NDIM>;
+  W v[HR::RPW][HR::EPL];
+  bool ok[HR::RPW][HR::EPL];
+  __device__ __forceinline__ void load(const W* __restrict__ base, Idx z0, Idx y0, Idx x0, Idx d0, Idx d1, Idx d2,
+                                       bool interior, W fill) {
+    using G = Geo<NDIM>;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const Idx plane = d1 * d2;
+    const W* org = base + ((z0 - G::ZH) * plane + (y0 - 1) * d2 + (x0 - 1));
 #pragma unroll
-    for (int k = 0; k < PPT; ++k) {
-      uint32_t m = f[k];
-      if (m == 0) continue;
-      uint32_t cur = ss[h[k]];
-      uint32_t best = cur;
+    for (int i = 0; i < HR::RPW; ++i) {
+      const int r = warp + i * (kRepairThreads / 32);
+      const int hz = r / G::HY, hy = r % G::HY;
+      const W* row = org + ((Idx)hz * plane + (Idx)hy * d2);
+      bool rowok = r < HR::R;
+      if (!interior) {
+        const Idx gz = z0 + hz - G::ZH, gy = y0 + hy - 1;
+        rowok = rowok && gz >= 0 && gz < d0 && gy >= 0 && gy < d1;
+      }
 #pragma unroll
-      for (int j = 0; j < 2 * D; ++j) {
-        if (m & (1u << j)) {
-          uint32_t v = ss[h[k] + slot_hoff<NDIM>(j)] + (j < D ? 1u : 0u);
-          best = v > best ? v : best;
+      for (int e = 0; e < HR::EPL; ++e) {
+        const int hx = lane + 32 * e;
+        bool o = rowok && hx < G::HX;
+        if (!interior) {
+          const Idx gx = x0 + hx - 1;
+          o = o && gx >= 0 && gx < d2;
         }
+        ok[i][e] = o;
+        v[i][e] = o ? __ldg(row + hx) : fill;
       }
-      if (best > cur) {
-        ss[h[k]] = best;
-        changed = 1;
-      }
-    }
-    ++it;
-    int any = __syncthreads_or(changed);
-    if (!any) {
-      *capped = false;
-      return it;
-    }
-    if (it >= max_inner) {
-      *capped = true;
-      return it;
     }
   }
-}
+};
 
-template <typename T, int NDIM>
-constexpr size_t quant_repair_smem() {
+template <int NDIM, typename Idx>
+__device__ __forceinline__ bool tile_interior(Idx z0, Idx y0, Idx x0, Idx d0, Idx d1, Idx d2) {
   using G = Geo<NDIM>;
-  return (size_t)G::HZ * G::HY * G::HX * (2 * sizeof(typename VT<T>::I) + 4) + 16;
+  return z0 - G::ZH >= 0 && z0 + G::TZ + G::ZH <= d0 && y0 >= 1 && y0 + G::TY + 1 <= d1 && x0 >= 1 &&
+         x0 + G::TX + 1 <= d2;
 }
 
 // ---------------------------------------------------------------------------
-// k_quant_repair: a1 + a2 + the first (tile-local) relaxation.
+// k_quant_flags: a1 (exact bins of the tile's points) + a2 (flags).
 // ---------------------------------------------------------------------------
 template <typename T, int NDIM>
-__global__ void __launch_bounds__(kRepairThreads, 2) k_quant_repair(RepairArgs a) {
+constexpr size_t quant_flags_smem() {
+  using G = Geo<NDIM>;
+  return (size_t)G::HZ * G::HY * G::HX * sizeof(typename VT<T>::I) + 16;
+}
+
+template <typename T, int NDIM, typename Idx>
+__global__ void __launch_bounds__(kRepairThreads, 3) k_quant_flags(RepairArgs a) {
   using G = Geo<NDIM>;
   using I = typename VT<T>::I;
   using U = typename VT<T>::U;
-  using Flag = typename G::Flag;
-  constexpr int HP = G::HZ * G::HY * G::HX;
+  using HR = HaloRows<NDIM>;
   constexpr int TP = G::TZ * G::TY * G::TX;
   constexpr int PPT = TP / kRepairThreads;
   constexpr int D = G::D;
-  constexpr int ZH = NDIM == 3 ? 1 : 0;  // halo depth in z
+  constexpr I kOut = (I)VT<T>::kSentinel;  // below every key: outside the grid
 
-  extern __shared__ __align__(16) uint8_t qr_smem[];
-  I* sbin = reinterpret_cast<I*>(qr_smem);
-  I* skey = sbin + HP;
-  uint32_t* ss = reinterpret_cast<uint32_t*>(skey + HP);
-  uint32_t& sdirs = ss[HP];
+  extern __shared__ __align__(16) uint8_t qf_smem[];
+  I* skey = reinterpret_cast<I*>(qf_smem);
 
-  const int64_t tile = blockIdx.x;
-  const int tx = (int)(tile % a.ntx), ty = (int)((tile / a.ntx) % a.nty), tz = (int)(tile / ((int64_t)a.ntx * a.nty));
-  const int64_t z0 = (int64_t)tz * G::TZ, y0 = (int64_t)ty * G::TY, x0 = (int64_t)tx * G::TX;
-  const T* X = static_cast<const T*>(a.x);
-  const I kNone = (I)VT<T>::kSentinel;  // escaped or outside the grid
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tx = blockIdx.x, ty = blockIdx.y, tz = blockIdx.z;  // 3D launch grid: no index division
+  const Idx d0 = (Idx)a.d0, d1 = (Idx)a.d1, d2 = (Idx)a.d2;
+  const Idx z0 = (Idx)tz * G::TZ, y0 = (Idx)ty * G::TY, x0 = (Idx)tx * G::TX;
+  const bool interior = tile_interior<NDIM, Idx>(z0, y0, x0, d0, d1, d2);
 
-  if (threadIdx.x == 0) sdirs = 0;
-  for (int hi = threadIdx.x; hi < HP; hi += kRepairThreads) {
-    int hx = hi % G::HX, hy = (hi / G::HX) % G::HY, hz = hi / (G::HX * G::HY);
-    int64_t gz = z0 + hz - ZH, gy = y0 + hy - 1, gx = x0 + hx - 1;
-    I b = kNone, k = 0;
-    if (gz >= 0 && gy >= 0 && gx >= 0 && gz < a.d0 && gy < a.d1 && gx < a.d2) {
-      T v = X[(gz * a.d1 + gy) * a.d2 + gx];
-      I q;
-      if (quantize<T>(v, a.eps, a.inv, q)) {
-        b = q;
-        k = (I)key_of((U)as_bits(v));
+  {
+    HaloLoad<NDIM, U, Idx> L;
+    L.load(static_cast<const U*>(a.x), z0, y0, x0, d0, d1, d2, interior, (U)0);
+#pragma unroll
+    for (int i = 0; i < HR::RPW; ++i) {
+      const int r = warp + i * (kRepairThreads / 32);
+#pragma unroll
+      for (int e = 0; e < HR::EPL; ++e) {
+        const int hx = lane + 32 * e;
+        if (r < HR::R && hx < G::HX) skey[r * G::HX + hx] = L.ok[i][e] ? (I)key_of(L.v[i][e]) : kOut;
       }
     }
-    sbin[hi] = b;
-    skey[hi] = k;
-    ss[hi] = 0;
   }
   __syncthreads();
 
-  uint32_t f[PPT];
-  int h[PPT];
-  bool inb[PPT];
+  // Warp w, step k handles tile row (w + 16k): lane = x.  Flags leave as one
+  // ballot per slot (bit plane), written by lane j as word j of the segment.
 #pragma unroll
   for (int k = 0; k < PPT; ++k) {
-    int lp = threadIdx.x + k * kRepairThreads;
-    int lx = lp % G::TX, ly = (lp / G::TX) % G::TY, lz = lp / (G::TX * G::TY);
-    h[k] = ((lz + ZH) * G::HY + (ly + 1)) * G::HX + (lx + 1);
-    inb[k] = (z0 + lz < a.d0) && (y0 + ly < a.d1) && (x0 + lx < a.d2);
+    const int row = warp + k * (kRepairThreads / 32);
+    const int lz = row / G::TY, ly = row % G::TY;
+    const int h = ((lz + G::ZH) * G::HY + (ly + 1)) * G::HX + (lane + 1);
+    const I kp = skey[h];
     uint32_t m = 0;
-    I bp = sbin[h[k]];
-    if (bp != kNone) {
-      I kp = skey[h[k]];
+    I b;
+    if (kp != kOut && quantize<T>(value_of_key<T>(kp), a.eps, a.inv, b)) {
+      const I kl = (I)key_of((U)as_bits(lo_t<T>((int64_t)b, a.eps)));
 #pragma unroll
       for (int j = 0; j < 2 * D; ++j) {
-        int hn = h[k] + slot_hoff<NDIM>(j);
-        // arc n -> p: same bin and n precedes p in SoS order.  A +e neighbour
-        // has the larger index, so it precedes p only with a smaller key; a -e
-        // neighbour precedes p on ties too (G4).
-        if (sbin[hn] == bp && (j < D ? skey[hn] < kp : skey[hn] <= kp)) m |= 1u << j;
+        const I kn = skey[h + slot_hoff<NDIM>(j)];
+        // n precedes p in SoS order within p's bin: bins are key intervals, so
+        // K_lo(p) <= key(n) < key(p) (+e slots) or <= key(p) (-e slots, G4)
+        const bool arc = kn >= kl && (j < D ? kn < kp : kn <= kp);
+        m |= (uint32_t)arc << j;
       }
     }
-    f[k] = m;
-  }
-
-  bool capped = false;
-  int iters = relax_tile<NDIM, PPT>(ss, f, h, a.max_inner, &capped);
-
-  // write flags and s; find boundary points with s > 0 that feed a neighbour
-  Flag* F = static_cast<Flag*>(a.flags);
-  uint32_t my_dirs = 0;
-  uint32_t my_max = 0;
+    uint32_t word = 0;
 #pragma unroll
-  for (int k = 0; k < PPT; ++k) {
-    if (!inb[k]) continue;
-    int lp = threadIdx.x + k * kRepairThreads;
-    int lx = lp % G::TX, ly = (lp / G::TX) % G::TY, lz = lp / (G::TX * G::TY);
-    int64_t gi = ((z0 + lz) * a.d1 + (y0 + ly)) * a.d2 + (x0 + lx);
-    uint32_t sv = ss[h[k]];
-    F[gi] = (Flag)f[k];
-    a.s[gi] = sv;
-    my_max = sv > my_max ? sv : my_max;
-    bool border = lx == 0 || lx == G::TX - 1 || ly == 0 || ly == G::TY - 1 ||
-                  (NDIM == 3 && (lz == 0 || lz == G::TZ - 1));
-    if (sv > 0 && border) {
-      I bp = sbin[h[k]], kp = skey[h[k]];
-#pragma unroll
-      for (int j = 0; j < 2 * D; ++j) {
-        int hn = h[k] + slot_hoff<NDIM>(j);
-        int hx = hn % G::HX, hy = (hn / G::HX) % G::HY, hz = hn / (G::HX * G::HY);
-        bool outside = hx == 0 || hx == G::HX - 1 || hy == 0 || hy == G::HY - 1 ||
-                       (NDIM == 3 && (hz == 0 || hz == G::HZ - 1));
-        // arc p -> n (p precedes n): the neighbour tile assumed s(p) = 0
-        if (outside && sbin[hn] == bp && (j < D ? kp <= skey[hn] : kp < skey[hn]))
-          my_dirs |= 1u << dir_of_halo<NDIM>(hz, hy, hx);
-      }
+    for (int j = 0; j < 2 * D; ++j) {
+      const uint32_t bj = __ballot_sync(0xffffffffu, (m >> j) & 1u);
+      if (lane == j) word = bj;
     }
+    const Idx gz = z0 + lz, gy = y0 + ly;
+    if (lane < G::SW && gz < d0 && gy < d1)
+      a.flags[((size_t)(gz * d1 + gy) * (size_t)a.nseg + (size_t)tx) * G::SW + lane] = word;
   }
-  if (my_dirs) atomicOr(&sdirs, my_dirs);
-  // warp-reduce max subbin for stats
-  for (int o = 16; o > 0; o >>= 1) {
-    uint32_t v = __shfl_xor_sync(0xffffffffu, my_max, o);
-    my_max = v > my_max ? v : my_max;
-  }
-  if ((threadIdx.x & 31) == 0 && my_max) atomicMax(&a.ctr->max_s, my_max);
-  __syncthreads();
-  uint32_t dirs = sdirs;
-  if (capped) dirs |= 1u << 13;  // self
-  enlist_dirs(a, dirs, tz, ty, tx, 1u);
-  if (threadIdx.x == 0) atomicAdd(&a.ctr->inner_iters, (unsigned long long)iters);
 }
 
 // ---------------------------------------------------------------------------
-// k_sweep: persistent passes over active tiles (cooperative launch).
+// k_sweep
 // ---------------------------------------------------------------------------
+template <int NDIM, typename Idx>
+__device__ __forceinline__ Idx slot_goff(int j, Idx plane, Idx d2) {
+  return (Idx)slot_dz<NDIM>(j) * plane + (Idx)slot_dy<NDIM>(j) * d2 + (Idx)slot_dx<NDIM>(j);
+}
+
+__device__ __forceinline__ uint32_t xshift(uint32_t v, int dx) {
+  // value of the neighbour at x + dx, placed at bit x
+  return dx > 0 ? (v >> 1) : (dx < 0 ? (v << 1) : v);
+}
+
+// Carry-lookahead fill along x: bit x is set if seed x is, or if mask bit x
+// is set and bit x-1 of the result is (the -x slot, weight 0).
+__device__ __forceinline__ uint32_t xfill(uint32_t g, uint32_t p) {
+  g |= p & (g << 1);
+  p &= p << 1;
+  g |= p & (g << 2);
+  p &= p << 2;
+  g |= p & (g << 4);
+  p &= p << 4;
+  g |= p & (g << 8);
+  p &= p << 8;
+  g |= p & (g << 16);
+  return g;
+}
+
+// flags of one point from its bit-plane segment
 template <int NDIM>
-__global__ void __launch_bounds__(kRepairThreads, 2) k_sweep(RepairArgs a) {
+__device__ __forceinline__ uint32_t point_flags(const uint32_t* seg, uint32_t bit) {
+  constexpr int SW = Geo<NDIM>::SW;
+  const uint4* s4 = reinterpret_cast<const uint4*>(seg);
+  uint32_t f = 0;
+#pragma unroll
+  for (int q = 0; q < SW / 4; ++q) {
+    const uint4 w = __ldg(s4 + q);
+    const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      if (4 * q + i < 2 * Geo<NDIM>::D) f |= ((ws[i] >> bit) & 1u) << (4 * q + i);
+  }
+  return f;
+}
+
+struct SweepSmem {
+  uint32_t cur[kSweepWarps][64];   // level rows being closed
+  uint32_t prev[kSweepWarps][64];  // Lev_{L-1} rows
+};
+
+template <int NDIM, typename Idx>
+__global__ void __launch_bounds__(kSweepThreads, 3) k_sweep(RepairArgs a) {
   namespace cg = cooperative_groups;
   using G = Geo<NDIM>;
-  using Flag = typename G::Flag;
-  constexpr int HP = G::HZ * G::HY * G::HX;
-  constexpr int TP = G::TZ * G::TY * G::TX;
-  constexpr int PPT = TP / kRepairThreads;
+  using UIdx = typename std::make_unsigned<Idx>::type;
   constexpr int D = G::D;
-  constexpr int ZH = NDIM == 3 ? 1 : 0;
+  constexpr int SW = G::SW;
+  constexpr int JX = D;  // the -x slot (0,0,-1): weight 0, closed by xfill
 
-  __shared__ uint32_t ss[HP];
-  __shared__ Flag sf[HP];
-  __shared__ uint8_t sraised[TP];
-  __shared__ uint32_t sdirs;
-  __shared__ uint32_t sn;
-
+  __shared__ SweepSmem S;
   cg::grid_group grid = cg::this_grid();
-  const Flag* F = static_cast<const Flag*>(a.flags);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  uint32_t* cur = S.cur[warp];
+  uint32_t* prv = S.prev[warp];
+  unsigned long long my_levels = 0;
+  unsigned my_raised = 0;
+  uint32_t my_max = 0;
+  const Idx d0 = (Idx)a.d0, d1 = (Idx)a.d1, d2 = (Idx)a.d2;
+  const Idx plane = d1 * d2;
+  const size_t nseg = (size_t)a.nseg;
+  const uint32_t ntx = (uint32_t)a.ntx, ntxy = (uint32_t)a.ntx * (uint32_t)a.nty;
 
-  for (int q = 1; q <= a.max_passes; ++q) {
-    if (threadIdx.x == 0) sn = *(volatile uint32_t*)&a.ctr->list_count[q % 3];
-    __syncthreads();
-    const uint32_t n = sn;
-    if (n == 0) break;
-    const uint32_t* L = a.lists + (size_t)(q % 3) * a.ntiles;
-    unsigned long long my_iters = 0;
-    for (uint32_t i = blockIdx.x; i < n; i += gridDim.x) {
-      const uint32_t tile = __ldcg(&L[i]);
-      const int tx = (int)(tile % a.ntx), ty = (int)((tile / a.ntx) % a.nty),
-                tz = (int)(tile / ((int64_t)a.ntx * a.nty));
-      const int64_t z0 = (int64_t)tz * G::TZ, y0 = (int64_t)ty * G::TY, x0 = (int64_t)tx * G::TX;
-      if (threadIdx.x == 0) sdirs = 0;
-      for (int hi = threadIdx.x; hi < HP; hi += kRepairThreads) {
-        int hx = hi % G::HX, hy = (hi / G::HX) % G::HY, hz = hi / (G::HX * G::HY);
-        int64_t gz = z0 + hz - ZH, gy = y0 + hy - 1, gx = x0 + hx - 1;
-        uint32_t sv = 0;
-        Flag fv = 0;
-        if (gz >= 0 && gy >= 0 && gx >= 0 && gz < a.d0 && gy < a.d1 && gx < a.d2) {
-          int64_t gi = (gz * a.d1 + gy) * a.d2 + gx;
-          sv = __ldcg(&a.s[gi]);
-          fv = F[gi];
-        }
-        ss[hi] = sv;
-        sf[hi] = fv;
-      }
-      __syncthreads();
-      uint32_t f[PPT], s_old[PPT];
-      int h[PPT];
+  // ---- pass 1: dense, one warp per tile, bit-parallel levels -----------------
+  const uint32_t gwarp = blockIdx.x * kSweepWarps + warp, nwarps = gridDim.x * kSweepWarps;
+  for (uint32_t tile = gwarp; tile < (uint32_t)a.ntiles; tile += nwarps) {
+    const uint32_t tz = tile / ntxy, rem = tile - tz * ntxy;
+    const uint32_t ty = rem / ntx, tx = rem - ty * ntx;
+    const Idx z0 = (Idx)tz * G::TZ, y0 = (Idx)ty * G::TY, x0 = (Idx)tx * G::TX;
+    const uint32_t vmask = x0 + 32 <= d2 ? 0xffffffffu : ((1u << (uint32_t)(d2 - x0)) - 1u);
+    // own rows rr = lane + 32*i: (lz, ly)
+    uint32_t F[2][2 * D];
+    int lz[2], ly[2];
+    bool rin[2];
 #pragma unroll
-      for (int k = 0; k < PPT; ++k) {
-        int lp = threadIdx.x + k * kRepairThreads;
-        int lx = lp % G::TX, ly = (lp / G::TX) % G::TY, lz = lp / (G::TX * G::TY);
-        h[k] = ((lz + ZH) * G::HY + (ly + 1)) * G::HX + (lx + 1);
-        f[k] = sf[h[k]];
-        s_old[k] = ss[h[k]];
-      }
-      bool capped = false;
-      my_iters += relax_tile<NDIM, PPT>(ss, f, h, a.max_inner, &capped);
+    for (int i = 0; i < 2; ++i) {
+      const int rr = lane + 32 * i;
+      lz[i] = rr / G::TY;
+      ly[i] = rr % G::TY;
+      rin[i] = z0 + lz[i] < d0 && y0 + ly[i] < d1;
+      const uint4* seg = reinterpret_cast<const uint4*>(
+          a.flags + ((size_t)((z0 + lz[i]) * d1 + (y0 + ly[i])) * nseg + tx) * SW);
 #pragma unroll
-      for (int k = 0; k < PPT; ++k) {
-        int lp = threadIdx.x + k * kRepairThreads;
-        uint32_t sv = ss[h[k]];
-        bool raised = sv != s_old[k];
-        sraised[lp] = raised;
-        if (raised) {
-          int lx = lp % G::TX, ly = (lp / G::TX) % G::TY, lz = lp / (G::TX * G::TY);
-          int64_t gi = ((z0 + lz) * a.d1 + (y0 + ly)) * a.d2 + (x0 + lx);
-          __stcg(&a.s[gi], sv);
-        }
-      }
-      __syncthreads();
-      // a halo point n fed (through its flags) by a raised tile point must
-      // be re-relaxed: enlist its tile for the next pass.
-      uint32_t my_dirs = 0;
-      for (int hi = threadIdx.x; hi < HP; hi += kRepairThreads) {
-        int hx = hi % G::HX, hy = (hi / G::HX) % G::HY, hz = hi / (G::HX * G::HY);
-        bool outside = hx == 0 || hx == G::HX - 1 || hy == 0 || hy == G::HY - 1 ||
-                       (NDIM == 3 && (hz == 0 || hz == G::HZ - 1));
-        uint32_t m = sf[hi];
-        if (!outside || m == 0) continue;
-        bool hit = false;
+      for (int q = 0; q < SW / 4; ++q) {
+        const uint4 w = rin[i] ? __ldg(seg + q) : make_uint4(0, 0, 0, 0);
+        const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
-        for (int j = 0; j < 2 * D; ++j) {
-          if (m & (1u << j)) {
-            int hp = hi + slot_hoff<NDIM>(j);
-            int px = hp % G::HX, py = (hp / G::HX) % G::HY, pz = hp / (G::HX * G::HY);
-            bool inside = px >= 1 && px <= G::TX && py >= 1 && py <= G::TY &&
-                          (NDIM == 2 || (pz >= 1 && pz <= G::TZ));
-            if (inside && sraised[((pz - ZH) * G::TY + (py - 1)) * G::TX + (px - 1)]) hit = true;
+        for (int t = 0; t < 4; ++t)
+          if (4 * q + t < 2 * D) F[i][4 * q + t] = ws[t];
+      }
+    }
+    uint32_t cnt[2][kLevelPlanes];
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int b = 0; b < kLevelPlanes; ++b) cnt[i][b] = 0;
+    uint32_t lev1[2] = {0, 0}, X[2] = {0, 0};
+    int L = 1;
+    for (;; ++L) {
+      uint32_t P[2];
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        uint32_t pv = 0;
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+          if (L == 1) {
+            pv |= F[i][j];  // from any predecessor (s >= 0) through a w = 1 arc
+          } else {
+            const int nz = lz[i] + slot_dz<NDIM>(j), ny = ly[i] + slot_dy<NDIM>(j);
+            const uint32_t v = (nz < G::TZ && ny < G::TY) ? prv[nz * G::TY + ny] : 0u;
+            pv |= F[i][j] & xshift(v, slot_dx<NDIM>(j));
           }
         }
-        if (hit) my_dirs |= 1u << dir_of_halo<NDIM>(hz, hy, hx);
+        P[i] = pv;
+        X[i] = xfill(pv, F[i][JX]);
       }
-      if (my_dirs) atomicOr(&sdirs, my_dirs);
-      __syncthreads();
-      uint32_t dirs = sdirs;
-      if (capped) dirs |= 1u << 13;
-      enlist_dirs(a, dirs, tz, ty, tx, (uint32_t)q + 1u);
-      __syncthreads();  // smem reuse by the next tile
+      // -e closure across rows (weight 0), Jacobi until stable
+      for (;;) {
+        cur[lane] = X[0];
+        cur[lane + 32] = X[1];
+        __syncwarp();
+        uint32_t Y[2];
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          uint32_t y = P[i];
+#pragma unroll
+          for (int j = D + 1; j < 2 * D; ++j) {
+            const int nz = lz[i] + slot_dz<NDIM>(j), ny = ly[i] + slot_dy<NDIM>(j);
+            const uint32_t v = (nz >= 0 && ny >= 0) ? cur[nz * G::TY + ny] : 0u;
+            y |= F[i][j] & xshift(v, slot_dx<NDIM>(j));
+          }
+          Y[i] = xfill(y, F[i][JX]);
+        }
+        const bool ch = (Y[0] != X[0]) || (Y[1] != X[1]);
+        X[0] = Y[0];
+        X[1] = Y[1];
+        __syncwarp();
+        if (!__any_sync(0xffffffffu, ch)) break;
+      }
+      if (!__any_sync(0xffffffffu, (X[0] | X[1]) != 0)) break;  // Lev_L empty: done
+      if (L == 1) {
+        lev1[0] = X[0];
+        lev1[1] = X[1];
+      }
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {  // bit-sliced count += Lev_L
+        uint32_t carry = X[i];
+#pragma unroll
+        for (int b = 0; b < kLevelPlanes; ++b) {
+          const uint32_t t = cnt[i][b] & carry;
+          cnt[i][b] ^= carry;
+          carry = t;
+        }
+      }
+      prv[lane] = X[0];
+      prv[lane + 32] = X[1];
+      __syncwarp();
+      if (L == kMaxLevel) break;  // hand the rest to the worklist
     }
-    if (threadIdx.x == 0) {
-      if (my_iters) atomicAdd(&a.ctr->inner_iters, my_iters);
-      if (blockIdx.x == 0) {
-        a.ctr->list_count[(q + 2) % 3] = 0;
-        a.ctr->passes = (unsigned long long)q;
-        a.ctr->tiles_processed += n;
+    const bool capped = L == kMaxLevel;
+    const int top = capped ? kMaxLevel : L - 1;  // highest non-empty level
+    const int nplanes = 32 - __clz(top | 1);
+    my_levels += (unsigned long long)L;
+    my_max = top > (int)my_max ? (uint32_t)top : my_max;
+    // write s row by row (lane = x)
+    for (int r = 0; r < 64; ++r) {
+      const int i = r >> 5, src = r & 31;
+      uint32_t sv = 0;
+#pragma unroll
+      for (int b = 0; b < kLevelPlanes; ++b) {
+        if (b < nplanes) {
+          const uint32_t pl = __shfl_sync(0xffffffffu, i ? cnt[1][b] : cnt[0][b], src);
+          sv |= ((pl >> lane) & 1u) << b;
+        }
       }
+      const int rz = r / G::TY, ry = r % G::TY;
+      const Idx gz = z0 + rz, gy = y0 + ry, gx = x0 + lane;
+      if (gz < d0 && gy < d1 && gx < d2) __stcg(&a.s[(gz * d1 + gy) * d2 + gx], sv);
+    }
+    // border points with s > 0 feed out-of-tile points that assumed s = 0
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const uint32_t lv = lev1[i] & vmask;
+      my_raised += __popc(lv);
+      if (!rin[i]) continue;
+      if (capped) {  // unfinished: continue point-wise from the top level
+        uint32_t c = X[i] & vmask;
+        while (c) {
+          const int x = __ffs(c) - 1;
+          c &= c - 1;
+          enqueue<Idx>(a, ((z0 + lz[i]) * d1 + (y0 + ly[i])) * d2 + x0 + x, 2);
+        }
+      }
+      if (!lv) continue;
+#pragma unroll
+      for (int j = 0; j < 2 * D; ++j) {
+        const int dz = slot_dz<NDIM>(j), dy = slot_dy<NDIM>(j), dx = slot_dx<NDIM>(j);
+        const int tlz = lz[i] + dz, tly = ly[i] + dy;
+        const bool row_in = tlz >= 0 && tlz < G::TZ && tly >= 0 && tly < G::TY;
+        uint32_t cand = row_in ? (lv & (dx > 0 ? 0x80000000u : (dx < 0 ? 1u : 0u))) : lv;
+        if (!cand) continue;
+        const Idx gz = z0 + tlz, gy = y0 + tly;
+        if (gz < 0 || gz >= d0 || gy < 0 || gy >= d1) continue;
+        const int jo = slot_opp<NDIM>(j);
+        const uint32_t* rowf = a.flags + ((size_t)(gz * d1 + gy) * nseg) * SW + jo;
+        uint32_t feed = 0;
+        const uint32_t inseg = cand & (dx > 0 ? 0x7fffffffu : (dx < 0 ? 0xfffffffeu : 0xffffffffu));
+        if (inseg) feed |= inseg & xshift(__ldg(rowf + (size_t)tx * SW), dx);
+        if (dx > 0 && (cand >> 31) && x0 + 32 < d2 && (__ldg(rowf + (size_t)(tx + 1) * SW) & 1u)) feed |= 0x80000000u;
+        if (dx < 0 && (cand & 1u) && tx > 0 && (__ldg(rowf + (size_t)(tx - 1) * SW) >> 31)) feed |= 1u;
+        while (feed) {
+          const int x = __ffs(feed) - 1;
+          feed &= feed - 1;
+          enqueue<Idx>(a, (gz * d1 + gy) * d2 + x0 + x + dx, 2);
+        }
+      }
+    }
+  }
+  if (tid == 0 && blockIdx.x == 0) a.ctr->pass_items[1] = (uint32_t)a.ntiles;
+  grid.sync();
+
+  // ---- passes >= 2: sparse, point-level ------------------------------------
+  const int gtid = blockIdx.x * kSweepThreads + tid, gthreads = gridDim.x * kSweepThreads;
+  int q = 2;
+  for (; q <= a.max_passes; ++q) {
+    const unsigned long long n = *(volatile unsigned long long*)&a.ctr->list_count[q % 3];
+    if (n == 0) break;
+    const UIdx* Lq = static_cast<const UIdx*>(a.plist) + (size_t)(q & 1) * a.cap;
+    for (unsigned long long i = gtid; i < n; i += gthreads) {
+      const Idx p = (Idx)__ldcg(&Lq[i]);
+      const uint32_t bit = 1u << ((uint32_t)p & 31u);
+      atomicAnd(&a.bitmap[(size_t)(q & 1) * a.bmw + ((UIdx)p >> 5)], ~bit);
+      const Idx z = p / plane, r2 = p - z * plane, y = r2 / d2, x = r2 - y * d2;
+      uint32_t fl = point_flags<NDIM>(a.flags + ((size_t)(z * d1 + y) * nseg + (size_t)(x >> 5)) * SW,
+                                      (uint32_t)x & 31u);
+      uint32_t best = 0;
+      while (fl) {
+        const int j = __ffs(fl) - 1;
+        fl &= fl - 1;
+        const int e = (j < D ? j : j - D) + 1;
+        const Idx off = (NDIM == 3 ? (Idx)(e >> 2) * plane : (Idx)0) + (Idx)((e >> 1) & 1) * d2 + (Idx)(e & 1);
+        const uint32_t v = j < D ? __ldcg(&a.s[p + off]) + 1u : __ldcg(&a.s[p - off]);
+        best = v > best ? v : best;
+      }
+      if (best <= __ldcg(&a.s[p])) continue;
+      const uint32_t old = atomicMax(&a.s[p], best);
+      if (old >= best) continue;
+      ++my_raised;
+      my_max = best > my_max ? best : my_max;
+#pragma unroll
+      for (int j = 0; j < 2 * D; ++j) {
+        const Idx qx = x + slot_dx<NDIM>(j), qy = y + slot_dy<NDIM>(j), qz = z + slot_dz<NDIM>(j);
+        if (qx < 0 || qx >= d2 || qy < 0 || qy >= d1 || qz < 0 || qz >= d0) continue;
+        const uint32_t w = __ldg(a.flags + ((size_t)(qz * d1 + qy) * nseg + (size_t)(qx >> 5)) * SW + slot_opp<NDIM>(j));
+        if ((w >> ((uint32_t)qx & 31u)) & 1u) enqueue<Idx>(a, p + slot_goff<NDIM, Idx>(j, plane, d2), q + 1);
+      }
+    }
+    if (tid == 0 && blockIdx.x == 0) {
+      a.ctr->list_count[(q + 2) % 3] = 0;
+      if (q < kPassHist) a.ctr->pass_items[q] = (uint32_t)n;
+      a.ctr->worklist_points += n;
     }
     grid.sync();
+  }
+  if (tid == 0 && blockIdx.x == 0) a.ctr->passes = (unsigned long long)(q - 1);
+  my_raised = __reduce_add_sync(0xffffffffu, my_raised);
+  my_max = __reduce_max_sync(0xffffffffu, my_max);
+  const unsigned lv32 = __reduce_add_sync(0xffffffffu, (unsigned)my_levels);
+  if (lane == 0 && lv32) atomicAdd(&a.ctr->inner_iters, (unsigned long long)lv32 / 32ull);
+  if (lane == 0 && my_raised) atomicAdd(&a.ctr->raised, (unsigned long long)my_raised);
+  if (lane == 0 && my_max) atomicMax(&a.ctr->max_s, my_max);
+}
+
+// Debug/parity: bit-plane flags -> one u16 per point.
+template <int NDIM>
+__global__ void k_unpack_flags(const uint32_t* flags, uint16_t* out, int64_t d0, int64_t d1, int64_t d2,
+                               int64_t nseg) {
+  const int64_t n = d0 * d1 * d2;
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t z = p / (d1 * d2), r = p - z * d1 * d2, y = r / d2, x = r - y * d2;
+    const uint32_t* seg = flags + ((z * d1 + y) * nseg + (x >> 5)) * Geo<NDIM>::SW;
+    uint32_t f = 0;
+    for (int j = 0; j < 2 * Geo<NDIM>::D; ++j) f |= ((seg[j] >> (x & 31)) & 1u) << j;
+    out[p] = (uint16_t)f;
   }
 }
 

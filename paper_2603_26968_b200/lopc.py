@@ -32,11 +32,11 @@ class LopcError(RuntimeError):
 
 
 class Stats(C.Structure):
-    _fields_ = [(n, C.c_uint64) for n in ("n_elems", "n_chunks", "n_tiles", "sweep_passes", "tiles_processed",
+    _fields_ = [(n, C.c_uint64) for n in ("n_elems", "n_chunks", "n_tiles", "sweep_passes", "worklist_points",
                                           "inner_iters", "escapes", "bin_bytes", "sub_bytes", "total_bytes")] + [
         ("max_subbin", C.c_uint32), ("timing_valid", C.c_uint32)] + [
         (n, C.c_float) for n in ("ms_h2d", "ms_quant_repair", "ms_sweep", "ms_encode", "ms_decode", "ms_d2h",
-                                 "ms_total")]
+                                 "ms_total")] + [("raised", C.c_uint64), ("pass_items", C.c_uint32 * 16)]
 
 
 _lib = None
@@ -206,4 +206,6 @@ def set_timing(on: bool = True):
 def last_stats() -> dict:
     st = Stats()
     load(False).lopc_last_stats(C.byref(st))
-    return {name: getattr(st, name) for name, _ in Stats._fields_}
+    d = {name: getattr(st, name) for name, _ in Stats._fields_}
+    d["pass_items"] = [int(v) for v in st.pass_items]
+    return d

@@ -107,7 +107,7 @@ def test_long_chains_cross_many_tiles(ref, gpu):
     gpu.compress(_t(x), 1.0)
     stats = gpu.last_stats()
     assert stats["total_bytes"] == len(st) and stats["max_subbin"] == 5999
-    assert stats["sweep_passes"] >= 6000 // 64 - 2  # the chain front advances about a tile per pass
+    assert stats["sweep_passes"] >= 2  # the chain crosses tiles: the sparse passes finish it
     x3 = (1.0 - 1e-7 * np.arange(9 * 17 * 70)).astype(np.float32).reshape(9, 17, 70)
     check_all(ref, gpu, x3, 1.0)
     x2 = np.full((40, 130), 0.5, np.float32)  # one plateau: all ties -> all zero
