@@ -117,11 +117,13 @@ typedef struct {
   float ms_total;             /* whole call on the stream */
   uint64_t raised;            /* subbins raised above 0 (dense pass) or raised again (sparse passes) */
   uint32_t pass_items[16];    /* [1]: tiles of the dense pass; [q>1]: worklist points of pass q */
+  uint64_t phase_cycles[16];  /* diagnostic (lopc_set_timing(2)): SM cycles per codec phase, summed over chunks */
 } lopc_stats;
 
 int lopc_last_stats(lopc_stats* out);
 
-/* Enable (1) / disable (0) per-kernel CUDA-event timing in lopc_stats. */
+/* Enable (1) / disable (0) per-kernel CUDA-event timing in lopc_stats; 2 also
+ * records per-phase clocks of the codec kernels (diagnostic, slower). */
 void lopc_set_timing(int enable);
 
 /* Message for a return code; lopc_last_error_string() adds CUDA detail. */

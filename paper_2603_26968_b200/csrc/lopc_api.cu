@@ -74,8 +74,15 @@ int check_eps(double eps) {
 
 inline size_t al(size_t v) { return (v + 255) & ~size_t(255); }
 
+// RN32(1/eps) for the f32 quantizer fast path; NaN disables it outside
+// 2^-120 < eps < 2^120.
+float inv32_of(double eps) {
+  if (!(eps > std::ldexp(1.0, -120) && eps < std::ldexp(1.0, 120))) return std::nanf("");
+  return (float)(1.0 / eps);
+}
+
 struct CLayout {
-  size_t ctr, bitmap, state, zero_end, plist, flags, s, stage_in, stage_out, total;
+  size_t ctr, bitmap, state, zero_end, plist, flags, s, stage, sizes, off, stage_in, stage_out, total;
   uint64_t bmw, nseg;
   int ntz, nty, ntx;
   uint64_t ntiles;
@@ -100,7 +107,7 @@ CLayout compress_layout(const Shape& s, bool host_in, bool host_out) {
   L.bitmap = o;
   o += al(2 * 4 * L.bmw);
   L.state = o;
-  o += al(8 * s.C);
+  o += al(8 * (s.C / kScanTile + 1));
   L.zero_end = o;
   L.plist = o;
   o += al(2 * (s.n < (1ull << 31) - (1ull << 24) ? 4 : 8) * s.n);
@@ -109,6 +116,12 @@ CLayout compress_layout(const Shape& s, bool host_in, bool host_out) {
   o += al(4ull * s.d0 * s.d1 * L.nseg * (s.ndims == 3 ? Geo<3>::SW : Geo<2>::SW));
   L.s = o;
   o += al(4 * s.n);
+  L.stage = o;
+  o += al(2ull * kChunkBytes * s.C);
+  L.sizes = o;
+  o += al(8 * s.C);
+  L.off = o;
+  o += al(8 * s.C);
   L.stage_in = o;
   if (host_in) o += al(s.k * s.n);
   L.stage_out = o;
@@ -140,10 +153,10 @@ int dev_info(DevInfo*& out) {
     g_dev = DevInfo{};
     g_dev.dev = dev;
     CK(cudaDeviceGetAttribute(&g_dev.sms, cudaDevAttrMultiProcessorCount, dev));
-    const int smem = (int)sizeof(CodecSmem);
+    const int smem = (int)sizeof(EncSmem), dsmem = (int)sizeof(DecSmem);
     CK(cudaFuncSetAttribute(k_encode<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     CK(cudaFuncSetAttribute(k_encode<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    CK(cudaFuncSetAttribute(k_decode, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    CK(cudaFuncSetAttribute(k_decode, cudaFuncAttributeMaxDynamicSharedMemorySize, dsmem));
 #define QRA(TT, ND)                                                                                      \
   CK(cudaFuncSetAttribute(k_quant_flags<TT, ND, int32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,     \
                           (int)quant_flags_smem<TT, ND>()));                                               \
@@ -155,7 +168,13 @@ int dev_info(DevInfo*& out) {
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_dev.occ_sweep3, k_sweep<3, int32_t>, kSweepThreads, 0));
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_dev.occ_sweep2w, k_sweep<2, int64_t>, kSweepThreads, 0));
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_dev.occ_sweep3w, k_sweep<3, int64_t>, kSweepThreads, 0));
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_dev.occ_decode, k_decode, kCodecThreads, smem));
+    {
+      cudaLaunchConfig_t cfg{};
+      cfg.gridDim = dim3(2 * 148 * 8, 1, 1);
+      cfg.blockDim = dim3(kCodecThreads, 1, 1);
+      cfg.dynamicSmemBytes = dsmem;
+      CK(cudaOccupancyMaxActiveClusters(&g_dev.occ_decode, k_decode, &cfg));  // whole GPU, clusters
+    }
     g_dev.attrs = true;
   }
   out = &g_dev;
@@ -241,6 +260,7 @@ int run_repair(const Shape& sh, const void* x, double eps, uint8_t* ws, const CL
   ra.ctr = reinterpret_cast<Counters*>(ws + L.ctr);
   ra.eps = eps;
   ra.inv = 1.0 / eps;
+  ra.inv32 = inv32_of(eps);
   ra.d0 = (int64_t)sh.d0;
   ra.d1 = (int64_t)sh.d1;
   ra.d2 = (int64_t)sh.d2;
@@ -353,7 +373,7 @@ size_t lopc_compress_workspace_bytes(int ndims, const uint64_t* dims, int dtype,
 
 size_t lopc_decompress_workspace_bytes(size_t in_bytes, size_t out_bytes, int host_io) {
   size_t cmax = in_bytes > kHdrBytes ? (in_bytes - kHdrBytes) / 16 + 1 : 1;
-  size_t t = al(sizeof(Counters)) + al(8 * cmax);
+  size_t t = al(sizeof(Counters)) + al(8 * (cmax / kScanTile + 1)) + al(8 * cmax);
   if (host_io) t += al(in_bytes) + al(out_bytes);
   return t;
 }
@@ -438,27 +458,59 @@ int lopc_compress_ex(const void* in, int ndims, const uint64_t* dims, int dtype,
   CK(cudaMemsetAsync(ws, 0, L.zero_end, st));
   if ((rc = run_repair(sh, x, eps, ws, L, st, tm, hc))) return rc;  // marks 2, 3
   uint8_t* dst = host_out ? ws + L.stage_out : static_cast<uint8_t*>(out);
+  Counters* dctr = reinterpret_cast<Counters*>(ws + L.ctr);
   EncodeArgs ea{};
   ea.x = x;
   ea.s = reinterpret_cast<const uint32_t*>(ws + L.s);
-  ea.out = dst;
-  ea.out_cap = host_out ? (kHdrBytes + 8 * sh.C + 2ull * kChunkBytes * sh.C) : cap;
-  ea.state = reinterpret_cast<uint64_t*>(ws + L.state);
-  ea.ctr = reinterpret_cast<Counters*>(ws + L.ctr);
+  ea.stage = ws + L.stage;
+  ea.sizes = reinterpret_cast<uint32_t*>(ws + L.sizes);
+  ea.ctr = dctr;
   ea.eps = eps;
   ea.inv = 1.0 / eps;
+  ea.inv32 = inv32_of(eps);
   ea.n = sh.n;
   ea.C = (uint32_t)sh.C;
   ea.ndims = sh.ndims;
   ea.vec = ((uintptr_t)x % 16 == 0) && ((uintptr_t)ea.s % 16 == 0);
+  ea.prof = g_timing >= 2;
   ea.d0 = sh.d0;
   ea.d1 = sh.d1;
   ea.d2 = sh.d2;
-  const size_t smem = sizeof(CodecSmem);
+  const size_t smem = sizeof(EncSmem);
   if (sh.dtype == LOPC_F32)
-    k_encode<float><<<(unsigned)sh.C, kCodecThreads, smem, st>>>(ea);
+    k_encode<float><<<(unsigned)(2 * sh.C), kCodecThreads, smem, st>>>(ea);
   else
-    k_encode<double><<<(unsigned)sh.C, kCodecThreads, smem, st>>>(ea);
+    k_encode<double><<<(unsigned)(2 * sh.C), kCodecThreads, smem, st>>>(ea);
+  CK(cudaGetLastError());
+  ScanArgs sa{};
+  sa.sizes = ea.sizes;
+  sa.C = (uint32_t)sh.C;
+  sa.off = reinterpret_cast<uint64_t*>(ws + L.off);
+  sa.state = reinterpret_cast<uint64_t*>(ws + L.state);
+  sa.ctr = dctr;
+  k_chunk_scan<<<(unsigned)((sh.C + kScanTile - 1) / kScanTile), kScanThreads, 0, st>>>(sa);
+  CK(cudaGetLastError());
+  PlaceArgs pa{};
+  pa.stage = ws + L.stage;
+  pa.sizes = ea.sizes;
+  pa.off = sa.off;
+  pa.out = dst;
+  pa.out_cap = host_out ? (kHdrBytes + 8 * sh.C + 2ull * kChunkBytes * sh.C) : cap;
+  pa.ctr = dctr;
+  pa.C = (uint32_t)sh.C;
+  pa.dtype = sh.dtype;
+  pa.ndims = sh.ndims;
+  pa.d0 = sh.d0;
+  pa.d1 = sh.d1;
+  pa.d2 = sh.d2;
+  pa.n = sh.n;
+  pa.eps = eps;
+  {
+    uint64_t pg = (sh.C + 7) / 8;
+    const uint64_t pmax = (uint64_t)di->sms * 8;
+    if (pg > pmax) pg = pmax;
+    k_place<<<(unsigned)pg, 256, 0, st>>>(pa);
+  }
   CK(cudaGetLastError());
   tm.mark();  // 4
   CK(cudaMemcpyAsync(hc, ws + L.ctr, sizeof(Counters), cudaMemcpyDeviceToHost, st));
@@ -474,6 +526,7 @@ int lopc_compress_ex(const void* in, int ndims, const uint64_t* dims, int dtype,
   g_stats.max_subbin = hc->max_s;
   g_stats.raised = hc->raised;
   for (int i = 0; i < 16; ++i) g_stats.pass_items[i] = hc->pass_items[i];
+  for (int i = 0; i < 16; ++i) g_stats.phase_cycles[i] = hc->phase[i];
   uint32_t err = hc->err;
   if (hc->passes >= (unsigned long long)(1 << 20) && hc->list_count[(hc->passes + 1) % 3] != 0) err |= kErrPassCap;
   if ((rc = map_err(err & ~kErrNoSpace))) return rc;
@@ -563,7 +616,8 @@ int lopc_decompress_ex(const void* in, size_t in_bytes, void* out, size_t out_ca
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const bool host_in = !is_device_ptr(in), host_out = !is_device_ptr(out);
   const size_t cmax = in_bytes > kHdrBytes ? (in_bytes - kHdrBytes) / 16 + 1 : 1;
-  size_t o_ctr = 0, o_state = al(sizeof(Counters)), o_in = o_state + al(8 * cmax);
+  const size_t ntile = cmax / kScanTile + 1;
+  size_t o_ctr = 0, o_state = al(sizeof(Counters)), o_off = o_state + al(8 * ntile), o_in = o_off + al(8 * cmax);
   size_t o_out = o_in + (host_in ? al(in_bytes) : 0);
   size_t need = o_out + (host_out ? al(out_capacity) : 0);
   if (!workspace || workspace_bytes < need) return LOPC_E_NOSPACE;
@@ -583,23 +637,34 @@ int lopc_decompress_ex(const void* in, size_t in_bytes, void* out, size_t out_ca
     src = ws + o_in;
   }
   tm.mark();  // 1
-  CK(cudaMemsetAsync(ws, 0, o_in, st));
+  CK(cudaMemsetAsync(ws, 0, o_off, st));
+  ScanArgs sa{};
+  sa.in = src;
+  sa.in_bytes = in_bytes;
+  sa.off = reinterpret_cast<uint64_t*>(ws + o_off);
+  sa.state = reinterpret_cast<uint64_t*>(ws + o_state);
+  sa.ctr = reinterpret_cast<Counters*>(ws + o_ctr);
+  sa.validate = 1;
+  sa.expect_total = in_bytes;
+  k_chunk_scan<<<(unsigned)ntile, kScanThreads, 0, st>>>(sa);
+  CK(cudaGetLastError());
   DecodeArgs da{};
   da.in = src;
   da.in_bytes = in_bytes;
   da.out = host_out ? (void*)(ws + o_out) : out;
   da.out_cap = out_capacity;
-  da.state = reinterpret_cast<uint64_t*>(ws + o_state);
+  da.off = sa.off;
   da.state_cap = cmax;
+  da.prof = g_timing >= 2;
   da.ctr = reinterpret_cast<Counters*>(ws + o_ctr);
-  unsigned grid = (unsigned)(di->occ_decode * di->sms);
-  if (grid > cmax) grid = (unsigned)cmax;
-  if (grid < 1) grid = 1;
-  k_decode<<<grid, kCodecThreads, sizeof(CodecSmem), st>>>(da);
+  unsigned grid = 2u * (unsigned)(di->occ_decode > 0 ? di->occ_decode : 1);
+  if (grid > 2 * cmax) grid = (unsigned)(2 * cmax);
+  k_decode<<<grid, kCodecThreads, sizeof(DecSmem), st>>>(da);
   CK(cudaGetLastError());
   tm.mark();  // 2
   CK(cudaMemcpyAsync(hc, ws + o_ctr, sizeof(Counters), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
+  for (int i = 0; i < 16; ++i) g_stats.phase_cycles[i] = hc->phase[i];
   if ((rc = map_err(hc->err))) return rc;
   if (host_out) {
     // N * k from the (validated) header

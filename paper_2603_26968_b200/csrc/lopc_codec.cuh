@@ -17,16 +17,16 @@
 
 namespace lopc {
 
-constexpr int kCodecThreads = 512;
+constexpr int kCodecThreads = 256;
 
 __device__ __forceinline__ int swz(int w) { return (w & ~31) | ((w ^ (w >> 5)) & 31); }
 
 // ---------------------------------------------------------------------------
-// Block-wide exclusive scan (sum) over kCodecThreads threads.
+// Block-wide exclusive scan (sum) over NT threads.
 // ---------------------------------------------------------------------------
-template <typename V>
+template <typename V, int NT = kCodecThreads>
 __device__ __forceinline__ V block_scan_excl(V v, V* wsum, V* total) {
-  constexpr int NW = kCodecThreads / 32;
+  constexpr int NW = NT / 32;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   V x = v;
 #pragma unroll
@@ -58,25 +58,29 @@ __device__ __forceinline__ uint32_t group_or(uint32_t v, int lanes) {
   return v;
 }
 
-// Non-zero-word bits of 16 bytes for word width g (16/g bits, LSB = first word).
-__device__ __forceinline__ uint32_t nz16(uint4 v, int g) {
-  if (g == 1) {
-    uint32_t r = 0;
-    uint32_t w4[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      uint32_t t = (((w4[i] & 0x7f7f7f7fu) + 0x7f7f7f7fu) | w4[i]) & 0x80808080u;
-      uint32_t n = ((t >> 7) & 1u) | ((t >> 14) & 2u) | ((t >> 21) & 4u) | ((t >> 28) & 8u);
-      r |= n << (4 * i);
-    }
-    return r;
-  }
-  if (g == 4) return (v.x != 0) | ((v.y != 0) << 1) | ((v.z != 0) << 2) | ((v.w != 0) << 3);
-  return ((v.x | v.y) != 0) | (((v.z | v.w) != 0) << 1);
-}
+// ---------------------------------------------------------------------------
+// RZE_g (Fig. 2; format DESIGN.md §4), block-parallel.
+//
+// A "unit" is 16 words of g bytes: it owns exactly bytes 2u and 2u+1 of the
+// first bitmap B0, so a thread with one unit knows its two B0 bytes, the B1
+// bits at those positions (B0[t] != B0[t-1]) and hence its K0 bytes; one
+// packed block scan gives every unit its K0 rank and its data rank.  B0 is
+// never materialised.  The small upper levels (B1 -> B2 -> B3: <= 272 bytes)
+// run on one warp with warp scans.
+// ---------------------------------------------------------------------------
+struct RzeScratch {
+  uint32_t b1[72];   // B1, <= 272 bytes
+  uint32_t b2[12];   // B2, <= 34 bytes
+  uint32_t b3[4];    // B3, <= 5 bytes
+  uint32_t pre1[72]; // decode: exclusive popcount prefix of B1 words
+  uint8_t k1[288];   // K1
+  uint8_t k2[48];    // K2
+  uint32_t wsum[32];
+  unsigned long long wsum64[32];
+  uint32_t info[8];
+};
 
-// RZE level sizes: sz[0] = ceil(n/8); while sz[i] > 8: sz[i+1] = ceil(sz[i]/8).
-__device__ __forceinline__ int rze_levels(uint32_t n, uint32_t* sz) {
+__device__ __forceinline__ int rze_sizes(uint32_t n, uint32_t* sz) {
   int top = 0;
   sz[0] = (n + 7) / 8;
   while (sz[top] > 8) {
@@ -86,112 +90,206 @@ __device__ __forceinline__ int rze_levels(uint32_t n, uint32_t* sz) {
   return top;
 }
 
-struct RzeSmem {
-  uint32_t bm0[768];  // up to 24576 input words
-  uint32_t bm1[96];
-  uint32_t bm2[16];
-  uint32_t bm3[4];
-  uint8_t kb0[3072];
-  uint8_t kb1[384];
-  uint8_t kb2[64];
-  uint32_t wsum[32];
-  unsigned long long wsum64[32];
-};
-
-__device__ __forceinline__ uint32_t* rze_bm(RzeSmem& r, int i) {
-  return i == 0 ? r.bm0 : (i == 1 ? r.bm1 : (i == 2 ? r.bm2 : r.bm3));
+// 4 bits: which bytes of w are non-zero
+__device__ __forceinline__ uint32_t nz4(uint32_t w) {
+  const uint32_t t = (((w & 0x7f7f7f7fu) + 0x7f7f7f7fu) | w) & 0x80808080u;
+  return (((t >> 7) * 0x00204081u) >> 21) & 0xfu;
 }
-__device__ __forceinline__ uint8_t* rze_kb(RzeSmem& r, int i) { return i == 0 ? r.kb0 : (i == 1 ? r.kb1 : r.kb2); }
 
-// RZE_g encode of `in` (shared, 16-byte aligned, L bytes; the bytes up to the
-// next multiple of 16 must be zero) into `out` (shared).  Returns the encoded
-// length; `out` is written only if that length <= out_limit.
-__device__ uint32_t rze_encode(const uint8_t* in, uint32_t L, int g, uint8_t* out, uint32_t out_limit, RzeSmem& r) {
-  const int tid = threadIdx.x, lane = tid & 31;
-  const uint32_t n = L / (uint32_t)g;
-  const int b = 16 / g;          // bits per thread per 16 bytes
-  const int lpw = 32 / b;        // lanes per bitmap word
-  const uint32_t L16 = (L + 15) & ~15u;
-  const int iters = (int)((L16 + kCodecThreads * 16 - 1) / (kCodecThreads * 16));
-  uint32_t masks[3] = {0, 0, 0}, ranks[3] = {0, 0, 0};
-  uint32_t running = 0;
-  for (int it = 0; it < iters; ++it) {
-    const uint32_t T = (uint32_t)(it * kCodecThreads + tid);
-    const uint32_t off = T * 16;
-    uint4 v = make_uint4(0, 0, 0, 0);
-    if (off < L16) v = *reinterpret_cast<const uint4*>(in + off);
-    uint32_t m = nz16(v, g);
-    uint32_t tot;
-    uint32_t ex = block_scan_excl<uint32_t>((uint32_t)__popc(m), r.wsum, &tot);
-    masks[it] = m;
-    ranks[it] = running + ex;
-    running += tot;
-    uint32_t word = group_or(m << ((T * b) & 31), lpw);
-    if ((lane % lpw) == 0) r.bm0[(T * b) >> 5] = word;
+// non-zero-word mask of 8 words of g bytes starting at p (16-byte aligned)
+__device__ __forceinline__ uint32_t nz_words8(const uint8_t* p, int g) {
+  if (g == 1) {
+    const uint2 v = *reinterpret_cast<const uint2*>(p);
+    return nz4(v.x) | (nz4(v.y) << 4);
   }
-  __syncthreads();
-  const uint32_t ndata = running;
-  uint32_t sz[6], ksz[6];
-  int top = 0;
-  sz[0] = (n + 7) / 8;
-  while (sz[top] > 8) {
-    sz[top + 1] = (sz[top] + 7) / 8;
-    const uint32_t* bi = rze_bm(r, top);
-    const uint8_t* bb = reinterpret_cast<const uint8_t*>(bi);
-    uint32_t* bn = rze_bm(r, top + 1);
-    uint8_t* kb = rze_kb(r, top);
-    const uint32_t nw = (sz[top] + 3) / 4;
-    uint32_t krun = 0;
-    for (uint32_t base = 0; base < nw; base += kCodecThreads) {
-      const uint32_t w = base + tid;
-      uint32_t m4 = 0;
-      uint32_t cur = 0;
-      if (w < nw) {
-        cur = bi[w];
-        uint32_t prev = w ? (uint32_t)bb[4 * w - 1] : 0u;
+  const uint4* q = reinterpret_cast<const uint4*>(p);
+  uint32_t m = 0;
+  if (g == 4) {
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          uint32_t byte = (cur >> (8 * j)) & 0xffu;
-          if (4 * w + j < sz[top] && byte != prev) m4 |= 1u << j;
-          prev = byte;
+    for (int k = 0; k < 2; ++k) {
+      const uint4 v = q[k];
+      m |= ((uint32_t)(v.x != 0) | ((uint32_t)(v.y != 0) << 1) | ((uint32_t)(v.z != 0) << 2) |
+            ((uint32_t)(v.w != 0) << 3)) << (4 * k);
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint4 v = q[k];
+      m |= ((uint32_t)((v.x | v.y) != 0) | ((uint32_t)((v.z | v.w) != 0) << 1)) << (2 * k);
+    }
+  }
+  return m;
+}
+
+// one warp: next bitmap level.  bi: si bytes; writes B_{i+1} bytes to bn and
+// K_i (bytes of bi whose B_{i+1} bit is set) to kb; returns |K_i|.
+__device__ __forceinline__ uint32_t level_up_warp(const uint8_t* bi, uint32_t si, uint8_t* bn, uint8_t* kb) {
+  const int lane = threadIdx.x & 31;
+  uint32_t kcount = 0;
+  for (uint32_t base = 0; base < si; base += 256) {
+    const uint32_t t0 = base + 8 * lane;
+    uint32_t bits = 0;
+    if (t0 < si) {
+      uint32_t prev = t0 ? bi[t0 - 1] : 0u;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        if (t0 + k < si) {
+          const uint32_t cur = bi[t0 + k];
+          bits |= (uint32_t)(cur != prev) << k;
+          prev = cur;
         }
       }
-      uint32_t tot;
-      uint32_t ex = block_scan_excl<uint32_t>((uint32_t)__popc(m4), r.wsum, &tot);
-      uint32_t k = krun + ex;
+      bn[t0 / 8] = (uint8_t)bits;
+    }
+    const uint32_t c = __popc(bits);
+    uint32_t incl = c;
 #pragma unroll
-      for (int j = 0; j < 4; ++j)
-        if (m4 & (1u << j)) kb[k++] = (uint8_t)(cur >> (8 * j));
-      krun += tot;
-      uint32_t word = group_or(m4 << ((w * 4) & 31), 8);
-      if ((lane & 7) == 0 && w < ((nw + 7) & ~7u)) bn[w >> 3] = word;
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
     }
-    __syncthreads();
-    ksz[top] = krun;
-    ++top;
+    uint32_t pos = kcount + incl - c;
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+      if ((bits >> k) & 1u) kb[pos++] = bi[t0 + k];
+    kcount += __shfl_sync(0xffffffffu, incl, 31);
   }
-  uint32_t total = sz[top] + (uint32_t)g * ndata;
-  for (int i = 0; i < top; ++i) total += ksz[i];
-  if (total <= out_limit) {
-    const uint8_t* bt = reinterpret_cast<const uint8_t*>(rze_bm(r, top));
-    if ((uint32_t)tid < sz[top]) out[tid] = bt[tid];
-    uint32_t off = sz[top];
-    for (int i = top - 1; i >= 0; --i) {
-      const uint8_t* kb = rze_kb(r, i);
-      for (uint32_t t = tid; t < ksz[i]; t += kCodecThreads) out[off + t] = kb[t];
-      off += ksz[i];
+  return kcount;
+}
+
+// one warp: rebuild bitmap level i from B_{i+1} (bn bytes) and K_i (kin):
+// B_i[t] = the last K byte selected at or before t (0 if none).  Returns |K_i|.
+__device__ __forceinline__ uint32_t level_down_warp(const uint8_t* bn, const uint8_t* kin, uint32_t si, uint8_t* bi) {
+  const int lane = threadIdx.x & 31;
+  uint32_t kcount = 0;
+  for (uint32_t base = 0; base < si; base += 256) {
+    const uint32_t t0 = base + 8 * lane;
+    uint32_t bits = t0 < si ? (uint32_t)bn[t0 / 8] : 0u;
+    if (t0 < si && si - t0 < 8) bits &= (1u << (si - t0)) - 1u;
+    const uint32_t c = __popc(bits);
+    uint32_t incl = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
     }
-    for (int it = 0; it < iters; ++it) {
-      const uint32_t T = (uint32_t)(it * kCodecThreads + tid);
-      uint32_t m = masks[it];
-      uint32_t k = ranks[it];
-      while (m) {
-        int j = __ffs(m) - 1;
-        m &= m - 1;
-        const uint8_t* src = in + T * 16 + j * g;
-        uint8_t* dst = out + off + k * g;
-        for (int q = 0; q < g; ++q) dst[q] = src[q];
-        ++k;
+    uint32_t r = kcount + incl - c;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      if (t0 + k < si) {
+        r += (bits >> k) & 1u;
+        bi[t0 + k] = r ? kin[r - 1] : (uint8_t)0;
+      }
+    }
+    kcount += __shfl_sync(0xffffffffu, incl, 31);
+  }
+  return kcount;
+}
+
+// RZE_g encode of `in` (shared, 16-byte aligned, L bytes, zero up to the next
+// multiple of 16g) into `out` (shared, any alignment).  Returns the encoded
+// length; `out` is written only if that length <= limit.
+__device__ uint32_t rze_enc(const uint8_t* in, uint32_t L, int g, uint8_t* out, uint32_t limit, RzeScratch& R) {
+  const int tid = threadIdx.x, lane = tid & 31;
+  const uint32_t n = L / (uint32_t)g;
+  uint32_t sz[6];
+  const int top = rze_sizes(n, sz);
+  const uint32_t units = (n + 15) / 16, ub = 16u * (uint32_t)g;
+  constexpr int MAXIT = 5;  // units per thread: <= 1088 units / 256 threads
+  uint32_t mk[MAXIT], rk[MAXIT];
+  uint32_t running = 0;
+  const int iters = (int)((units + kCodecThreads - 1) / kCodecThreads);
+#pragma unroll
+  for (int it = 0; it < MAXIT; ++it) {
+    if (it >= iters) break;
+    const uint32_t u = (uint32_t)(it * kCodecThreads + tid);
+    uint32_t m = 0, prevb = 0;
+    if (u < units) {
+      const uint8_t* p = in + u * ub;
+      m = nz_words8(p, g) | (nz_words8(p + 8 * g, g) << 8);
+      prevb = u ? nz_words8(p - 8 * g, g) : 0u;
+    }
+    const uint32_t lo = m & 0xffu, hi = m >> 8;
+    uint32_t b1 = 0;
+    if (top >= 1 && u < units) b1 = (uint32_t)(lo != prevb) | ((uint32_t)(hi != lo && 2 * u + 1 < sz[0]) << 1);
+    uint32_t tot;
+    const uint32_t ex = block_scan_excl<uint32_t>((uint32_t)__popc(m) | ((uint32_t)__popc(b1) << 20), R.wsum, &tot);
+    mk[it] = m | (b1 << 16);
+    rk[it] = running + ex;
+    running += tot;
+    if (top >= 1) {
+      const uint32_t w = group_or(b1 << (2 * (u & 15)), 16);
+      if ((lane & 15) == 0 && u < units) R.b1[u >> 4] = w;
+    }
+  }
+  const uint32_t ndata = running & 0xfffffu, nk0 = running >> 20;
+  __syncthreads();
+  if (tid < 32) {
+    uint32_t k2n = 0, k1n = 0;
+    const uint8_t* b1 = reinterpret_cast<const uint8_t*>(R.b1);
+    const uint8_t* b2 = reinterpret_cast<const uint8_t*>(R.b2);
+    if (top >= 2) k1n = level_up_warp(b1, sz[1], reinterpret_cast<uint8_t*>(R.b2), R.k1);
+    __syncwarp();
+    if (top >= 3) k2n = level_up_warp(b2, sz[2], reinterpret_cast<uint8_t*>(R.b3), R.k2);
+    __syncwarp();
+    uint32_t o = sz[top];
+    const uint32_t o2 = o;
+    if (top >= 3) o += k2n;
+    const uint32_t o1 = o;
+    if (top >= 2) o += k1n;
+    const uint32_t koff = o;
+    const uint32_t doff = koff + nk0;
+    const uint32_t total = doff + (uint32_t)g * ndata;
+    if (total <= limit && top >= 1) {
+      const uint8_t* bt = top == 1 ? b1 : (top == 2 ? b2 : reinterpret_cast<const uint8_t*>(R.b3));
+      if ((uint32_t)lane < sz[top]) out[lane] = bt[lane];
+      if (top >= 3)
+        for (uint32_t t = lane; t < k2n; t += 32) out[o2 + t] = R.k2[t];
+      if (top >= 2)
+        for (uint32_t t = lane; t < k1n; t += 32) out[o1 + t] = R.k1[t];
+    }
+    if (lane == 0) {
+      R.info[0] = koff;
+      R.info[1] = doff;
+      R.info[2] = total;
+    }
+  }
+  __syncthreads();
+  const uint32_t koff = R.info[0], doff = R.info[1], total = R.info[2];
+  if (total <= limit) {
+#pragma unroll
+    for (int it = 0; it < MAXIT; ++it) {
+      if (it >= iters) break;
+      const uint32_t u = (uint32_t)(it * kCodecThreads + tid);
+      if (u >= units) continue;
+      const uint32_t m = mk[it] & 0xffffu, b1 = mk[it] >> 16;
+      uint32_t dr = rk[it] & 0xfffffu;
+      const uint32_t kr = rk[it] >> 20;
+      if (top == 0) {  // B0 itself is the top level (<= 8 bytes)
+        if (2 * u < sz[0]) out[2 * u] = (uint8_t)(m & 0xffu);
+        if (2 * u + 1 < sz[0]) out[2 * u + 1] = (uint8_t)(m >> 8);
+      } else {
+        uint32_t k = koff + kr;
+        if (b1 & 1u) out[k++] = (uint8_t)(m & 0xffu);
+        if (b1 & 2u) out[k] = (uint8_t)(m >> 8);
+      }
+      const uint8_t* p = in + u * ub;
+      uint8_t* d = out + doff;
+      if (g == 1) {
+        const uint4 v = *reinterpret_cast<const uint4*>(p);
+        const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          if ((m >> j) & 1u) d[dr++] = (uint8_t)(w4[j >> 2] >> (8 * (j & 3)));
+        }
+      } else {
+#pragma unroll 4
+        for (int j = 0; j < 16; ++j) {
+          if ((m >> j) & 1u) {
+            for (int q = 0; q < g; ++q) d[(size_t)dr * g + q] = p[j * g + q];
+            ++dr;
+          }
+        }
       }
     }
   }
@@ -199,96 +297,134 @@ __device__ uint32_t rze_encode(const uint8_t* in, uint32_t L, int g, uint8_t* ou
   return total;
 }
 
-// RZE_g decode: `in` (shared) holds in_len payload bytes; reconstructs L bytes
-// into `out` (shared, 16-byte aligned, room for L rounded up to 16).  Returns
-// the number of payload bytes consumed, or 0xffffffff if the payload is too
-// short for its bitmaps (corrupt).
-__device__ uint32_t rze_decode(const uint8_t* in, uint32_t in_len, uint32_t L, int g, uint8_t* out, RzeSmem& r) {
+// RZE_g decode: `in` (shared, any alignment) holds in_len payload bytes;
+// reconstructs L bytes into `out` (shared, 16-byte aligned, room for L
+// rounded up to 16g).  Returns the payload bytes consumed, or 0xffffffff if
+// the payload is too short for what its bitmaps announce (corrupt).
+__device__ uint32_t rze_dec(const uint8_t* in, uint32_t in_len, uint32_t L, int g, uint8_t* out, RzeScratch& R) {
   const int tid = threadIdx.x;
   const uint32_t n = L / (uint32_t)g;
   uint32_t sz[6];
-  const int top = rze_levels(n, sz);
-  if (sz[top] > in_len) return 0xffffffffu;
-  {
-    uint8_t* bt = reinterpret_cast<uint8_t*>(rze_bm(r, top));
-    if ((uint32_t)tid < ((sz[top] + 3) & ~3u)) bt[tid] = (uint32_t)tid < sz[top] ? in[tid] : 0;
+  const int top = rze_sizes(n, sz);
+  const uint32_t units = (n + 15) / 16, ub = 16u * (uint32_t)g;
+  if (tid < 32) {
+    const int lane = tid;
+    bool ok = sz[top] <= in_len;
+    uint32_t pos = sz[top];
+    uint8_t* b1 = reinterpret_cast<uint8_t*>(R.b1);
+    uint8_t* b2 = reinterpret_cast<uint8_t*>(R.b2);
+    uint8_t* b3 = reinterpret_cast<uint8_t*>(R.b3);
+    if (ok && top >= 1) {
+      uint8_t* bt = top == 1 ? b1 : (top == 2 ? b2 : b3);
+      if ((uint32_t)lane < sz[top]) bt[lane] = in[lane];
+      __syncwarp();
+      if (top >= 3) {
+        const uint32_t k2n = level_down_warp(b3, in + pos, sz[2], b2);
+        pos += k2n;
+        ok = ok && pos <= in_len;
+        __syncwarp();
+      }
+      if (ok && top >= 2) {
+        const uint32_t k1n = level_down_warp(b2, in + pos, sz[1], b1);
+        pos += k1n;
+        ok = ok && pos <= in_len;
+        __syncwarp();
+      }
+      // exclusive popcount prefix of B1 words, bits < sz0 only
+      const uint32_t nw1 = (sz[0] + 31) / 32;
+      uint32_t carry = 0;
+      for (uint32_t base = 0; base < nw1; base += 32) {
+        const uint32_t w = base + lane;
+        uint32_t c = 0;
+        if (w < nw1) {
+          uint32_t word = (uint32_t)b1[4 * w] | ((uint32_t)b1[4 * w + 1] << 8) | ((uint32_t)b1[4 * w + 2] << 16) |
+                          ((uint32_t)b1[4 * w + 3] << 24);
+          if (sz[0] - 32 * w < 32) word &= (1u << (sz[0] - 32 * w)) - 1u;
+          R.b1[w] = word;
+          c = __popc(word);
+        }
+        uint32_t incl = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += y;
+        }
+        if (w < nw1) R.pre1[w] = carry + incl - c;
+        carry += __shfl_sync(0xffffffffu, incl, 31);
+      }
+      const uint32_t koff = pos;
+      pos += carry;  // |K0|
+      ok = ok && pos <= in_len;
+      if (lane == 0) R.info[0] = koff;
+    }
+    if (lane == 0) {
+      R.info[1] = top == 0 ? sz[0] : pos;
+      R.info[2] = ok;
+    }
   }
   __syncthreads();
-  uint32_t pos = sz[top];
-  for (int i = top - 1; i >= 0; --i) {
-    const uint32_t* bn = rze_bm(r, i + 1);
-    uint32_t* bi = rze_bm(r, i);
-    const uint32_t nw = (sz[i] + 3) / 4;
-    uint32_t krun = 0;
-    for (uint32_t base = 0; base < nw; base += kCodecThreads) {
-      const uint32_t w = base + tid;
-      uint32_t m4 = 0;
-      if (w < nw) {
-        m4 = (bn[w >> 3] >> ((w & 7) * 4)) & 0xfu;
-        uint32_t valid = sz[i] - 4 * w;  // >= 1
-        if (valid < 4) m4 &= (1u << valid) - 1u;
-      }
-      uint32_t tot;
-      uint32_t ex = block_scan_excl<uint32_t>((uint32_t)__popc(m4), r.wsum, &tot);
-      if (pos + krun + tot > in_len) return 0xffffffffu;  // block-uniform
-      if (w < nw) {
-        uint32_t k = krun + ex;  // selected positions before this word
-        uint32_t word = 0;
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          if (m4 & (1u << j)) ++k;
-          uint32_t byte = k ? (uint32_t)in[pos + k - 1] : 0u;
-          if (4 * w + j >= sz[i]) byte = 0;
-          word |= byte << (8 * j);
-        }
-        bi[w] = word;
-      }
-      krun += tot;
-    }
+  if (!R.info[2]) {
     __syncthreads();
-    pos += krun;
+    return 0xffffffffu;
   }
-  // words
-  const int b = 16 / g;
-  const uint32_t L16 = (L + 15) & ~15u;
-  const int iters = (int)((L16 + kCodecThreads * 16 - 1) / (kCodecThreads * 16));
+  const uint32_t koff = R.info[0], doff = R.info[1];
+  constexpr int MAXIT = 5;
+  const int iters = (int)((units + kCodecThreads - 1) / kCodecThreads);
   uint32_t running = 0;
-  for (int it = 0; it < iters; ++it) {
-    const uint32_t T = (uint32_t)(it * kCodecThreads + tid);
+  bool bad = false;
+#pragma unroll
+  for (int it = 0; it < MAXIT; ++it) {
+    if (it >= iters) break;
+    const uint32_t u = (uint32_t)(it * kCodecThreads + tid);
     uint32_t m = 0;
-    if (T * 16 < L16) {
-      m = (r.bm0[(T * b) >> 5] >> ((T * b) & 31)) & ((1u << b) - 1u);
-      uint32_t first = T * (uint32_t)b;
-      if (first >= n)
-        m = 0;
-      else if (n - first < (uint32_t)b)
-        m &= (1u << (n - first)) - 1u;
+    if (u < units) {
+      uint32_t lo, hi;
+      const uint32_t t0 = 2 * u, t1 = 2 * u + 1;
+      if (top == 0) {
+        lo = t0 < sz[0] && t0 < in_len ? in[t0] : 0u;
+        hi = t1 < sz[0] && t1 < in_len ? in[t1] : 0u;
+      } else {
+        const uint32_t w0 = R.b1[t0 >> 5];
+        const uint32_t r0 = R.pre1[t0 >> 5] + __popc(w0 & ((2u << (t0 & 31)) - 1u));
+        const uint32_t r1 = r0 + ((w0 >> (t1 & 31)) & 1u);  // t0, t1 share a B1 word
+        lo = r0 ? in[koff + r0 - 1] : 0u;
+        hi = t1 < sz[0] ? (r1 ? in[koff + r1 - 1] : 0u) : 0u;
+      }
+      m = lo | (hi << 8);
+      if (16 * u + 16 > n) m &= (1u << (n - 16 * u)) - 1u;
     }
     uint32_t tot;
-    uint32_t ex = block_scan_excl<uint32_t>((uint32_t)__popc(m), r.wsum, &tot);
-    if (pos + (uint32_t)g * (running + tot) > in_len) return 0xffffffffu;
-    if (T * 16 < L16) {
-      uint32_t k = running + ex;
-      uint8_t tmp[16];
+    uint32_t dr = running + block_scan_excl<uint32_t>((uint32_t)__popc(m), R.wsum, &tot);
+    running += tot;
+    if (doff + (uint32_t)g * running > in_len) bad = true;  // block-uniform
+    if (!bad && u < units) {
+      const uint8_t* src = in + doff;
+      uint8_t* dst = out + u * ub;
+      if (g == 1) {
+        uint32_t w4[4] = {0, 0, 0, 0};
 #pragma unroll
-      for (int q = 0; q < 16; ++q) tmp[q] = 0;
-      for (int j = 0; j < b; ++j) {
-        if (m & (1u << j)) {
-          for (int q = 0; q < g; ++q) tmp[j * g + q] = in[pos + k * g + q];
-          ++k;
+        for (int j = 0; j < 16; ++j)
+          if ((m >> j) & 1u) w4[j >> 2] |= (uint32_t)src[dr++] << (8 * (j & 3));
+        *reinterpret_cast<uint4*>(dst) = make_uint4(w4[0], w4[1], w4[2], w4[3]);
+      } else {
+        uint32_t* d32 = reinterpret_cast<uint32_t*>(dst);
+#pragma unroll 4
+        for (int j = 0; j < 16; ++j) {
+          for (int q = 0; q < g / 4; ++q) {
+            uint32_t v = 0;
+            if ((m >> j) & 1u) {
+              const uint8_t* b = src + (size_t)dr * g + 4 * q;
+              v = (uint32_t)b[0] | ((uint32_t)b[1] << 8) | ((uint32_t)b[2] << 16) | ((uint32_t)b[3] << 24);
+            }
+            d32[j * (g / 4) + q] = v;
+          }
+          dr += (m >> j) & 1u;
         }
       }
-      uint4 v;
-      v.x = tmp[0] | (tmp[1] << 8) | (tmp[2] << 16) | ((uint32_t)tmp[3] << 24);
-      v.y = tmp[4] | (tmp[5] << 8) | (tmp[6] << 16) | ((uint32_t)tmp[7] << 24);
-      v.z = tmp[8] | (tmp[9] << 8) | (tmp[10] << 16) | ((uint32_t)tmp[11] << 24);
-      v.w = tmp[12] | (tmp[13] << 8) | (tmp[14] << 16) | ((uint32_t)tmp[15] << 24);
-      *reinterpret_cast<uint4*>(out + T * 16) = v;
     }
-    running += tot;
   }
   __syncthreads();
-  return pos + (uint32_t)g * running;
+  return bad ? 0xffffffffu : doff + (uint32_t)g * running;
 }
 
 // ---------------------------------------------------------------------------
@@ -309,16 +445,32 @@ __device__ __forceinline__ void transpose32(uint32_t (&A)[32]) {
   }
 }
 
-// BIT_k (G20): words (swizzled shared) -> 8k planes of W bits (linear bytes).
 template <typename U>
-__device__ __forceinline__ void bit_forward(const U* words, uint32_t* planes, int W) {
+__host__ __device__ constexpr U nb_mask() {
+  return (U)0xAAAAAAAAAAAAAAAAull;
+}
+
+// BIT_k (G20): words (swizzled shared) -> 8k planes of W bits (linear bytes),
+// run by threads [t0, t0 + nt).  With DIFF, word i is first replaced by
+// NB(w[i] - w[i-1]) (DIFFNB_k, G18/G19), computed on the fly.
+template <typename U, bool DIFF>
+__device__ __forceinline__ void bit_forward(const U* words, uint32_t* planes, int W, int t0, int nt) {
   const int groups = W / 32;
-  for (int g = threadIdx.x; g < groups; g += kCodecThreads) {
+  for (int g = (int)threadIdx.x - t0; g >= 0 && g < groups; g += nt) {
 #pragma unroll
     for (int half = 0; half < (int)sizeof(U) / 4; ++half) {
       uint32_t A[32];
+      U prev = (DIFF && g) ? words[swz(32 * g - 1)] : (U)0;
 #pragma unroll
-      for (int i = 0; i < 32; ++i) A[i] = (uint32_t)(words[swz(32 * g + i)] >> (32 * half));
+      for (int i = 0; i < 32; ++i) {
+        U w = words[swz(32 * g + i)];
+        if (DIFF) {
+          const U cur = w;
+          w = (U)(((U)(cur - prev) + nb_mask<U>()) ^ nb_mask<U>());
+          prev = cur;
+        }
+        A[i] = (uint32_t)(w >> (32 * half));
+      }
       transpose32(A);
 #pragma unroll
       for (int j = 0; j < 32; ++j) planes[(32 * half + j) * groups + g] = A[j];
@@ -326,10 +478,11 @@ __device__ __forceinline__ void bit_forward(const U* words, uint32_t* planes, in
   }
 }
 
+// inverse, by threads [t0, t0 + nt)
 template <typename U>
-__device__ __forceinline__ void bit_inverse(const uint32_t* planes, U* words, int W) {
+__device__ __forceinline__ void bit_inverse(const uint32_t* planes, U* words, int W, int t0, int nt) {
   const int groups = W / 32;
-  for (int g = threadIdx.x; g < groups; g += kCodecThreads) {
+  for (int g = (int)threadIdx.x - t0; g >= 0 && g < groups; g += nt) {
 #pragma unroll
     for (int half = 0; half < (int)sizeof(U) / 4; ++half) {
       uint32_t A[32];
@@ -347,9 +500,56 @@ __device__ __forceinline__ void bit_inverse(const uint32_t* planes, U* words, in
   }
 }
 
+// In-place BIT_k / BIT_k^-1 on one shared buffer (words swizzled <-> planes
+// linear): every (group, 32-bit half) item is staged in registers, then the
+// block synchronises, then the results are stored.  All threads must call.
+template <typename U, bool DIFF>
+__device__ __forceinline__ void bit_forward_inplace(uint8_t* buf, int W) {
+  const int groups = W / 32, items = groups * (int)(sizeof(U) / 4);
+  const int t = threadIdx.x, g = t % groups, half = t / groups;
+  const U* words = reinterpret_cast<const U*>(buf);
+  uint32_t A[32];
+  if (t < items) {
+    U prev = (DIFF && g) ? words[swz(32 * g - 1)] : (U)0;
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      U w = words[swz(32 * g + i)];
+      if (DIFF) {
+        const U cur = w;
+        w = (U)(((U)(cur - prev) + nb_mask<U>()) ^ nb_mask<U>());
+        prev = cur;
+      }
+      A[i] = (uint32_t)(w >> (32 * half));
+    }
+    transpose32(A);
+  }
+  __syncthreads();
+  if (t < items) {
+    uint32_t* planes = reinterpret_cast<uint32_t*>(buf);
+#pragma unroll
+    for (int j = 0; j < 32; ++j) planes[(32 * half + j) * groups + g] = A[j];
+  }
+  __syncthreads();
+}
+
 template <typename U>
-__host__ __device__ constexpr U nb_mask() {
-  return (U)0xAAAAAAAAAAAAAAAAull;
+__device__ __forceinline__ void bit_inverse_inplace(uint8_t* buf, int W) {
+  const int groups = W / 32, items = groups * (int)(sizeof(U) / 4);
+  const int t = threadIdx.x, g = t % groups, half = t / groups;
+  uint32_t A[32];
+  if (t < items) {
+    const uint32_t* planes = reinterpret_cast<const uint32_t*>(buf);
+#pragma unroll
+    for (int j = 0; j < 32; ++j) A[j] = planes[(32 * half + j) * groups + g];
+    transpose32(A);
+  }
+  __syncthreads();
+  if (t < items) {
+    uint32_t* w32 = reinterpret_cast<uint32_t*>(buf);
+#pragma unroll
+    for (int i = 0; i < 32; ++i) w32[swz(32 * g + i) * (int)(sizeof(U) / 4) + half] = A[i];
+  }
+  __syncthreads();
 }
 
 // ---------------------------------------------------------------------------
@@ -358,29 +558,19 @@ __host__ __device__ constexpr U nb_mask() {
 struct EncodeArgs {
   const void* x;
   const uint32_t* s;
-  uint8_t* out;
-  uint64_t out_cap;
-  uint64_t* state;  // look-back state per chunk
+  uint8_t* stage;    // C x 32 KiB staging slots (workspace)
+  uint32_t* sizes;   // 2C: (bin_size, sub_size)
   Counters* ctr;
   double eps, inv;
   uint64_t n;
   uint32_t C;
   int ndims;
   int vec;  // x and s are 16-byte aligned: vector loads allowed
+  float inv32;  // RN32(1/eps) for the f32 fast path, NaN = off
+  int prof;     // diagnostic phase clocks
   uint64_t d0, d1, d2;
 };
 
-struct CodecSmem {
-  alignas(16) uint8_t wb[kChunkBytes];      // bin words (swizzled)
-  alignas(16) uint8_t ws[kChunkBytes];      // subbin words (swizzled)
-  alignas(16) uint8_t z[17408];             // DIFFNB words / RZE_k output
-  alignas(16) uint8_t sh[kChunkBytes];      // bit planes
-  alignas(16) uint8_t ob[kChunkBytes + 16]; // bin payload
-  alignas(16) uint8_t os[kChunkBytes + 16]; // subbin payload
-  RzeSmem r;
-  uint32_t misc[8];
-  unsigned long long misc64[4];
-};
 
 constexpr uint64_t kFlagAgg = 1ull << 62, kFlagIncl = 2ull << 62, kValMask = (1ull << 62) - 1;
 
@@ -419,176 +609,333 @@ __device__ __forceinline__ uint64_t lookback_warp(uint64_t* state, uint32_t c, u
 
 __device__ __forceinline__ uint32_t pad4(uint32_t v) { return (v + 3u) & ~3u; }
 
+// One CTA per (chunk, stream): blockIdx.x = 2c + role, role 0 = bins, 1 = subbins.
+struct EncSmem {
+  alignas(16) uint8_t Wd[kChunkBytes + 64];  // words -> planes (in place) -> [subbins] payload
+  alignas(16) uint8_t O[17408 + 128];        // [bins] payload | [subbins] a4 queue, RZE_k output
+  RzeScratch R;
+  uint32_t misc[4];
+};
+
 template <typename T>
-__global__ void __launch_bounds__(kCodecThreads, 2) k_encode(EncodeArgs a) {
+__global__ void __launch_bounds__(kCodecThreads, 5) k_encode(EncodeArgs a) {
   using U = typename VT<T>::U;
   using I = typename VT<T>::I;
   constexpr int K = VT<T>::K;
   constexpr int W = kChunkBytes / K;
-  constexpr int PER = W / kCodecThreads;  // words per thread (8 f32, 4 f64)
+  constexpr int PER = W / kCodecThreads;  // words per thread (16 f32, 8 f64)
   extern __shared__ __align__(16) uint8_t smem_raw[];
-  CodecSmem& sm = *reinterpret_cast<CodecSmem*>(smem_raw);
-  U* WB = reinterpret_cast<U*>(sm.wb);
-  U* WS = reinterpret_cast<U*>(sm.ws);
-  U* Z = reinterpret_cast<U*>(sm.z);
-  const int tid = threadIdx.x;
-
-  if (tid == 0) sm.misc[0] = atomicAdd(&a.ctr->ticket, 1u);
-  __syncthreads();
-  const uint32_t c = sm.misc[0];
+  EncSmem& sm = *reinterpret_cast<EncSmem*>(smem_raw);
+  U* WD = reinterpret_cast<U*>(sm.Wd);
+  uint16_t* Q = reinterpret_cast<uint16_t*>(sm.O);
+  const int tid = threadIdx.x, lane = tid & 31;
+  const uint32_t c = blockIdx.x >> 1;
+  const bool subs = blockIdx.x & 1;
+  PhaseClock pc;
+  pc.start(a.prof);
+  if (tid == 0) sm.misc[0] = 0;  // a4 queue length
   const uint64_t e0 = (uint64_t)c * W;
   const uint32_t cnt = (uint32_t)min((uint64_t)W, a.n - e0);
   const T* X = static_cast<const T*>(a.x) + e0;
   const uint32_t* S = a.s + e0;
+  __syncthreads();
 
-  // --- a1 + a4: re-quantize, words, bound self-check ---------------------
-  // each thread owns PER/4 runs of 4 consecutive words, loaded as 16-byte vectors
-  uint32_t esc = 0, bad = 0;
+  // --- a1: re-quantize; bin words (role 0) or subbin words + a4 queue (role 1).
+  // Thread slot k = 4v + q holds element 4 (v * NT + tid) + q.
+  constexpr int NV = PER / 2;  // two halves of PER slots (register budget)
+  uint32_t escm = 0, qmask = 0;
+#pragma unroll 1
+  for (int hh = 0; hh < 2; ++hh) {
+    T xs[NV];
+    uint32_t ss[NV];
+    if (a.vec && cnt == (uint32_t)W) {
 #pragma unroll
-  for (int v = 0; v < PER / 4; ++v) {
-    const int i0 = 4 * (v * kCodecThreads + tid);
-    T xs[4];
-    uint32_t ss[4];
-    if (a.vec && (uint32_t)i0 + 3 < cnt) {
-      if constexpr (sizeof(T) == 4) {
-        const float4 xv = __ldg(reinterpret_cast<const float4*>(X + i0));
-        xs[0] = xv.x, xs[1] = xv.y, xs[2] = xv.z, xs[3] = xv.w;
-      } else {
-        const double2 x0 = __ldg(reinterpret_cast<const double2*>(X + i0));
-        const double2 x1 = __ldg(reinterpret_cast<const double2*>(X + i0 + 2));
-        xs[0] = x0.x, xs[1] = x0.y, xs[2] = x1.x, xs[3] = x1.y;
-      }
-      const uint4 sv = __ldg(reinterpret_cast<const uint4*>(S + i0));
-      ss[0] = sv.x, ss[1] = sv.y, ss[2] = sv.z, ss[3] = sv.w;
-    } else {
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const bool in = (uint32_t)(i0 + q) < cnt;
-        xs[q] = in ? X[i0 + q] : (T)0;
-        ss[q] = in ? S[i0 + q] : 0u;
-      }
-    }
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int i = i0 + q;
-      U bw = 0, sw = 0;
-      if ((uint32_t)i < cnt) {
-        const T x = xs[q];
-        const uint32_t sq = ss[q];
-        I b;
-        if (quantize<T>(x, a.eps, a.inv, b)) {
-          bw = (U)b;
-          sw = (U)sq;
-          if (sq != 0) {
-            // x^ = value with key(lo(b)) + s must not exceed x (a4)
-            const T lo = lo_t<T>((int64_t)b, a.eps);
-            if ((int64_t)key_of((U)as_bits(lo)) + (int64_t)sq > (int64_t)key_of((U)as_bits(x))) bad = 1;
-          }
+      for (int v = 0; v < NV / 4; ++v) {
+        const int i0 = 4 * ((hh * (NV / 4) + v) * kCodecThreads + tid);
+        if constexpr (sizeof(T) == 4) {
+          const float4 xv = __ldg(reinterpret_cast<const float4*>(X + i0));
+          xs[4 * v] = xv.x, xs[4 * v + 1] = xv.y, xs[4 * v + 2] = xv.z, xs[4 * v + 3] = xv.w;
         } else {
-          bw = VT<T>::kSentinel;
-          sw = (U)as_bits(x);
-          ++esc;
+          const double2 x0 = __ldg(reinterpret_cast<const double2*>(X + i0));
+          const double2 x1 = __ldg(reinterpret_cast<const double2*>(X + i0 + 2));
+          xs[4 * v] = x0.x, xs[4 * v + 1] = x0.y, xs[4 * v + 2] = x1.x, xs[4 * v + 3] = x1.y;
+        }
+        if (subs) {
+          const uint4 sv = __ldg(reinterpret_cast<const uint4*>(S + i0));
+          ss[4 * v] = sv.x, ss[4 * v + 1] = sv.y, ss[4 * v + 2] = sv.z, ss[4 * v + 3] = sv.w;
         }
       }
-      WB[swz(i)] = bw;
-      WS[swz(i)] = sw;
-    }
-  }
-  if (bad) atomicOr(&a.ctr->err, kErrBound);
-  esc = __reduce_add_sync(0xffffffffu, esc);
-  if ((tid & 31) == 0 && esc) atomicAdd(&a.ctr->escapes, (unsigned long long)esc);
-  __syncthreads();
-
-  // --- a5: bins: DIFFNB_k -> BIT_k -> RZE_1 -----------------------------------
+    } else {
 #pragma unroll
-  for (int v = 0; v < PER; ++v) {
-    const int i = v * kCodecThreads + tid;
-    U cur = WB[swz(i)];
-    U prev = i ? WB[swz(i - 1)] : (U)0;
-    U d = cur - prev;
-    Z[swz(i)] = (U)((d + nb_mask<U>()) ^ nb_mask<U>());
-  }
-  __syncthreads();
-  bit_forward<U>(Z, reinterpret_cast<uint32_t*>(sm.sh), W);
-  __syncthreads();
-  const uint32_t blen = rze_encode(sm.sh, kChunkBytes, 1, sm.ob, kChunkBytes - 4, sm.r);
-  const uint32_t bsize = blen <= kChunkBytes - 4 ? pad4(blen) : kChunkBytes;
-  if (bsize < kChunkBytes && (uint32_t)tid < bsize - blen) sm.ob[blen + tid] = 0;
-
-  // --- a6: subbins: BIT_k -> RZE_k -> RZE_1 ----------------------------------
-  bit_forward<U>(WS, reinterpret_cast<uint32_t*>(sm.sh), W);
-  __syncthreads();
-  const uint32_t l1 = rze_encode(sm.sh, kChunkBytes, K, sm.z, 0xffffffffu, sm.r);
-  if ((uint32_t)tid < 16) sm.z[l1 + tid] = 0;  // zero tail for the next stage's 16-byte reads
-  __syncthreads();
-  const uint32_t l2 = rze_encode(sm.z, l1, 1, sm.os + 2, kChunkBytes - 6, sm.r);
-  const uint32_t ssize = l2 <= kChunkBytes - 6 ? pad4(2 + l2) : kChunkBytes;
-  if (ssize < kChunkBytes) {
-    if (tid == 0) {
-      sm.os[0] = (uint8_t)(l1 & 0xffu);
-      sm.os[1] = (uint8_t)(l1 >> 8);
+      for (int k = 0; k < NV; ++k) {
+        const int i = 4 * ((hh * (NV / 4) + (k >> 2)) * kCodecThreads + tid) + (k & 3);
+        const bool in = (uint32_t)i < cnt;
+        xs[k] = in ? X[i] : (T)0;
+        ss[k] = (in && subs) ? S[i] : 0u;
+      }
     }
-    if ((uint32_t)tid < ssize - 2 - l2) sm.os[2 + l2 + tid] = 0;
-  }
-
-  // --- a7: placement by decoupled look-back -----------------------------------
-  if (tid < 32) {
-    const uint64_t excl = lookback_warp(a.state, c, (uint64_t)bsize + ssize);
-    if (tid == 0) sm.misc64[0] = excl;
-  }
-  __syncthreads();
-  const uint64_t base = (uint64_t)kHdrBytes + 8ull * a.C + sm.misc64[0];
-  const uint64_t end = base + bsize + ssize;
-  const bool fits = end <= a.out_cap;
-  if (tid == 0) {
-    if (!fits) atomicOr(&a.ctr->err, kErrNoSpace);
-    if ((uint64_t)kHdrBytes + 8ull * (c + 1) <= a.out_cap) {
-      uint32_t* tab = reinterpret_cast<uint32_t*>(a.out + kHdrBytes + 8ull * c);
-      tab[0] = bsize;
-      tab[1] = ssize;
-    }
-    atomicAdd(&a.ctr->bin_bytes, (unsigned long long)bsize);
-    atomicAdd(&a.ctr->sub_bytes, (unsigned long long)ssize);
-    if (c == a.C - 1) {
-      a.ctr->total_bytes = end;
-      if (a.out_cap >= kHdrBytes) {
-        uint32_t* h32 = reinterpret_cast<uint32_t*>(a.out);
-        uint64_t* h64 = reinterpret_cast<uint64_t*>(a.out);
-        h32[0] = 0x43504f4cu;  // "LOPC"
-        h32[1] = 1u | ((uint32_t)(K == 4 ? 0 : 1) << 16) | ((uint32_t)a.ndims << 24);
-        h64[1] = a.d0;
-        h64[2] = a.d1;
-        h64[3] = a.d2;
-        h64[4] = (uint64_t)__double_as_longlong(a.eps);
-        h64[5] = a.n;
-        h32[12] = kChunkBytes;
-        h32[13] = a.C;
-        h64[7] = end;
+#pragma unroll
+    for (int v = 0; v < NV / 4; ++v) {  // groups of 4: fast attempt, rare exact fix-up, words
+      I bb[4];
+      uint32_t slow = 0;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) slow |= (uint32_t)!qtry(xs[4 * v + q], a.inv32, a.inv, bb[q]) << q;
+      if (slow) {  // rare: near a half-integer, escapes, huge bins
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          if ((slow >> q) & 1u) {
+            const int64_t r = quantize_slow<T>(xs[4 * v + q], a.eps, a.inv);
+            if (r == kEscape) escm |= 1u << (hh * NV + 4 * v + q);
+            bb[q] = (I)r;
+          }
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int k = 4 * v + q, kk = hh * NV + k;
+        const int i = 4 * ((hh * (NV / 4) + v) * kCodecThreads + tid) + q;
+        const bool in = (uint32_t)i < cnt, e = (escm >> kk) & 1u;
+        U w;
+        if (subs) {
+          w = e ? (U)as_bits(xs[k]) : (U)ss[k];
+          qmask |= (uint32_t)(!e && ss[k] != 0) << kk;
+        } else {
+          w = e ? VT<T>::kSentinel : (U)bb[q];
+        }
+        WD[swz(i)] = in ? w : (U)0;
       }
     }
   }
-  if (!fits) return;
-  uint32_t* dst = reinterpret_cast<uint32_t*>(a.out + base);
-  if (bsize == kChunkBytes) {
-    for (int i = tid; i < W; i += kCodecThreads) {
-      U w = WB[swz(i)];
+  if (subs) {  // a4 queue: one warp scan per thread-mask
+    const uint32_t nq = __popc(qmask);
+    uint32_t incl = nq;
 #pragma unroll
-      for (int h = 0; h < K / 4; ++h) dst[i * (K / 4) + h] = (uint32_t)(w >> (32 * h));
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    uint32_t base = 0;
+    if (lane == 31 && incl) base = atomicAdd(&sm.misc[0], incl);
+    base = __shfl_sync(0xffffffffu, base, 31) + incl - nq;
+    for (uint32_t m = qmask; m; m &= m - 1) {
+      const int k = __ffs(m) - 1;
+      Q[base++] = (uint16_t)(4 * ((k >> 2) * kCodecThreads + tid) + (k & 3));
     }
   } else {
-    const uint32_t* src = reinterpret_cast<const uint32_t*>(sm.ob);
-    for (uint32_t i = tid; i < bsize / 4; i += kCodecThreads) dst[i] = src[i];
+    const uint32_t esc = __reduce_add_sync(0xffffffffu, (uint32_t)__popc(escm));
+    if (lane == 0 && esc) atomicAdd(&a.ctr->escapes, (unsigned long long)esc);
   }
-  dst += bsize / 4;
-  if (ssize == kChunkBytes) {
+  __syncthreads();
+  pc.mark(a.ctr, 1);
+
+  uint32_t size;
+  if (subs) {
+    // --- a4: bound self-check of the queued points: key(lo(b)) + s <= key(x)
+    const uint32_t nq = sm.misc[0];
+    uint32_t bad = 0;
+    for (uint32_t q = tid; q < nq; q += kCodecThreads) {
+      const int i = Q[q];
+      const T x = X[i];
+      I b = 0;
+      if (!qtry(x, a.inv32, a.inv, b)) b = (I)quantize_slow<T>(x, a.eps, a.inv);
+      const uint32_t sq = (uint32_t)WD[swz(i)];
+      const T lo = lo_t<T>((int64_t)b, a.eps);
+      if ((int64_t)key_of((U)as_bits(lo)) + (int64_t)sq > (int64_t)key_of((U)as_bits(x))) bad = 1;
+    }
+    if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(&a.ctr->err, kErrBound);
+    pc.mark(a.ctr, 2);
+    // --- a6: subbins: BIT_k -> RZE_k -> RZE_1 ----------------------
+    bit_forward_inplace<U, false>(sm.Wd, W);
+    pc.mark(a.ctr, 3);
+    const uint32_t l1 = rze_enc(sm.Wd, kChunkBytes, K, sm.O, 0xffffffffu, sm.R);
+    for (uint32_t t = l1 + tid; t < ((l1 + 15) & ~15u) + 16; t += kCodecThreads) sm.O[t] = 0;
+    __syncthreads();
+    pc.mark(a.ctr, 5);
+    const uint32_t l2 = rze_enc(sm.O, l1, 1, sm.Wd + 2, kChunkBytes - 6, sm.R);
+    size = l2 <= kChunkBytes - 6 ? pad4(2 + l2) : kChunkBytes;
+    if (size < kChunkBytes) {
+      if (tid == 0) {
+        sm.Wd[0] = (uint8_t)(l1 & 0xffu);
+        sm.Wd[1] = (uint8_t)(l1 >> 8);
+      }
+      if ((uint32_t)tid < size - 2 - l2) sm.Wd[2 + l2 + tid] = 0;
+    }
+    pc.mark(a.ctr, 6);
+  } else {
+    // --- a5: bins: DIFFNB_k -> BIT_k -> RZE_1 -------------------
+    bit_forward_inplace<U, true>(sm.Wd, W);
+    pc.mark(a.ctr, 3);
+    const uint32_t l = rze_enc(sm.Wd, kChunkBytes, 1, sm.O, kChunkBytes - 4, sm.R);
+    size = l <= kChunkBytes - 4 ? pad4(l) : kChunkBytes;
+    if (size < kChunkBytes && (uint32_t)tid < size - l) sm.O[l + tid] = 0;
+    pc.mark(a.ctr, 4);
+  }
+  __syncthreads();
+
+  // --- a7 (part 1): the payload goes to this chunk's staging slot (bins at
+  // +0, subbins at +16 KiB); k_chunk_scan + k_place put it in the stream.
+  if (tid == 0) {
+    a.sizes[2 * c + (subs ? 1 : 0)] = size;
+    atomicAdd(subs ? &a.ctr->sub_bytes : &a.ctr->bin_bytes, (unsigned long long)size);
+  }
+  uint32_t* dst = reinterpret_cast<uint32_t*>(a.stage + (size_t)c * 2 * kChunkBytes + (subs ? kChunkBytes : 0));
+  if (size == kChunkBytes) {
+    // raw fallback (G23): rebuild the words (the buffer now holds planes)
     for (int i = tid; i < W; i += kCodecThreads) {
-      U w = WS[swz(i)];
+      U w = 0;
+      if ((uint32_t)i < cnt) {
+        I b;
+        if (quantize_fast<T>(X[i], a.inv32, a.eps, a.inv, b))
+          w = subs ? (U)S[i] : (U)b;
+        else
+          w = subs ? (U)as_bits(X[i]) : VT<T>::kSentinel;
+      }
 #pragma unroll
       for (int h = 0; h < K / 4; ++h) dst[i * (K / 4) + h] = (uint32_t)(w >> (32 * h));
     }
   } else {
-    const uint32_t* src = reinterpret_cast<const uint32_t*>(sm.os);
-    for (uint32_t i = tid; i < ssize / 4; i += kCodecThreads) dst[i] = src[i];
+    const uint4* src = reinterpret_cast<const uint4*>(subs ? sm.Wd : sm.O);
+    uint4* d4 = reinterpret_cast<uint4*>(dst);
+    for (uint32_t i = tid; i < (size + 15) / 16; i += kCodecThreads) d4[i] = src[i];
+  }
+  __syncthreads();
+  pc.mark(a.ctr, 7);
+}
+
+// ---------------------------------------------------------------------------
+// k_chunk_scan: a7 (part 2), the one prefix sum of the stream format: chunk
+// payload offsets = exclusive scan of (bin_size + sub_size).  Decoupled
+// look-back over tiles of 2048 chunks (each tile's aggregate is available at
+// once, so the look-back never waits long).  In decode mode the sizes come
+// from the stream's table and are validated.
+// ---------------------------------------------------------------------------
+constexpr int kScanThreads = 512;
+constexpr int kScanPer = 4;
+constexpr int kScanTile = kScanThreads * kScanPer;
+
+struct ScanArgs {
+  const uint32_t* sizes;  // 2C u32: (bin_size, sub_size) pairs (encode mode)
+  const uint8_t* in;      // decode mode: the stream (C and the table come from it)
+  uint64_t in_bytes;
+  uint32_t C;             // encode mode
+  uint64_t* off;          // out: C payload offsets
+  uint64_t* state;        // per-tile look-back state (zeroed)
+  Counters* ctr;
+  int validate;           // decode: check 4 <= size <= 16384, size % 4 == 0
+  uint64_t expect_total;  // decode: the stream length
+};
+
+__global__ void __launch_bounds__(kScanThreads) k_chunk_scan(ScanArgs a) {
+  __shared__ unsigned long long wsum[32];
+  __shared__ unsigned long long excl_s;
+  __shared__ uint32_t tile_s;
+  __shared__ uint32_t C_s;
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    tile_s = atomicAdd(&a.ctr->ticket2, 1u);
+    uint32_t C = a.C;
+    if (a.in) {  // decode: C from the header, bounded by the stream length
+      C = 0;
+      if (a.in_bytes >= kHdrBytes && reinterpret_cast<const uint32_t*>(a.in)[0] == 0x43504f4cu) {
+        C = reinterpret_cast<const uint32_t*>(a.in)[13];
+        if ((uint64_t)kHdrBytes + 8ull * C > a.in_bytes) C = 0;
+      }
+    }
+    C_s = C;
+  }
+  __syncthreads();
+  const uint32_t tile = tile_s, C = C_s;
+  if ((uint64_t)tile * kScanTile >= C) return;  // beyond the last tile: nobody waits on it
+  const uint32_t* sizes = a.in ? reinterpret_cast<const uint32_t*>(a.in + kHdrBytes) : a.sizes;
+  const uint64_t base = (uint64_t)kHdrBytes + 8ull * C;
+  const uint32_t c0 = tile * kScanTile + tid * kScanPer;
+  unsigned long long v[kScanPer];
+  unsigned long long run = 0;
+  bool bad = false;
+#pragma unroll
+  for (int k = 0; k < kScanPer; ++k) {
+    v[k] = 0;
+    const uint32_t c = c0 + k;
+    if (c < C) {
+      const uint32_t bs = sizes[2 * c], ss = sizes[2 * c + 1];
+      if (a.validate && !(bs >= 4 && bs <= kChunkBytes && (bs & 3u) == 0 && ss >= 4 && ss <= kChunkBytes &&
+                          (ss & 3u) == 0))
+        bad = true;
+      v[k] = (unsigned long long)bs + ss;
+    }
+    run += v[k];
+  }
+  if (bad) atomicOr(&a.ctr->err, kErrCorrupt);
+  unsigned long long tot;
+  const unsigned long long ex = block_scan_excl<unsigned long long, kScanThreads>(run, wsum, &tot);
+  if (tid < 32) {
+    const uint64_t e = lookback_warp(a.state, tile, tot);
+    if (tid == 0) excl_s = e;
+  }
+  __syncthreads();
+  unsigned long long o = base + excl_s + ex;
+#pragma unroll
+  for (int k = 0; k < kScanPer; ++k) {
+    const uint32_t c = c0 + k;
+    if (c < C) {
+      a.off[c] = o;
+      o += v[k];
+      if (c == C - 1) {
+        a.ctr->total_bytes = o;
+        if (a.validate && o != a.expect_total) atomicOr(&a.ctr->err, kErrCorrupt);
+      }
+    }
+  }
+}
+
+// k_place: a7 (part 3) — move each staged chunk to its offset, write the
+// size table and the header.  One warp per chunk.
+struct PlaceArgs {
+  const uint8_t* stage;
+  const uint32_t* sizes;
+  const uint64_t* off;
+  uint8_t* out;
+  uint64_t out_cap;
+  Counters* ctr;
+  uint32_t C;
+  int dtype, ndims;
+  uint64_t d0, d1, d2, n;
+  double eps;
+};
+
+__global__ void __launch_bounds__(256) k_place(PlaceArgs a) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t total = a.ctr->total_bytes;
+  if (total > a.out_cap) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(&a.ctr->err, kErrNoSpace);
+    return;
+  }
+  const uint32_t nw = gridDim.x * (blockDim.x / 32);
+  for (uint32_t c = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); c < a.C; c += nw) {
+    const uint32_t bs = a.sizes[2 * c], ss = a.sizes[2 * c + 1];
+    const uint32_t* src = reinterpret_cast<const uint32_t*>(a.stage + (size_t)c * 2 * kChunkBytes);
+    uint32_t* dst = reinterpret_cast<uint32_t*>(a.out + a.off[c]);
+    for (uint32_t i = lane; i < bs / 4; i += 32) dst[i] = __ldcs(&src[i]);
+    for (uint32_t i = lane; i < ss / 4; i += 32) dst[bs / 4 + i] = __ldcs(&src[kChunkBytes / 4 + i]);
+    if (lane == 0) {
+      uint32_t* tab = reinterpret_cast<uint32_t*>(a.out + kHdrBytes + 8ull * c);
+      tab[0] = bs;
+      tab[1] = ss;
+    }
+    if (c == 0 && lane == 0) {
+      uint32_t* h32 = reinterpret_cast<uint32_t*>(a.out);
+      uint64_t* h64 = reinterpret_cast<uint64_t*>(a.out);
+      h32[0] = 0x43504f4cu;  // "LOPC"
+      h32[1] = 1u | ((uint32_t)a.dtype << 16) | ((uint32_t)a.ndims << 24);
+      h64[1] = a.d0;
+      h64[2] = a.d1;
+      h64[3] = a.d2;
+      h64[4] = (uint64_t)__double_as_longlong(a.eps);
+      h64[5] = a.n;
+      h32[12] = kChunkBytes;
+      h32[13] = a.C;
+      h64[7] = total;
+    }
   }
 }
 
@@ -600,9 +947,10 @@ struct DecodeArgs {
   uint64_t in_bytes;
   void* out;
   uint64_t out_cap;
-  uint64_t* state;
-  uint64_t state_cap;  // entries available
+  const uint64_t* off;  // chunk payload offsets from k_chunk_scan
+  uint64_t state_cap;   // chunk entries available in the workspace
   Counters* ctr;
+  int prof;             // diagnostic phase clocks
 };
 
 struct Hdr {
@@ -655,172 +1003,187 @@ __device__ __forceinline__ Hdr parse_header(const DecodeArgs& a) {
   return h;
 }
 
+// One CTA per (chunk, stream), the two CTAs of a chunk form a 2-CTA cluster:
+// rank 0 decodes the bins, rank 1 the subbins, each into its own shared
+// memory; after a cluster barrier each CTA reconstructs half of the chunk,
+// reading the partner's words through distributed shared memory.
+struct DecSmem {
+  alignas(16) uint8_t Wd[kChunkBytes + 64];  // payload (subbins) -> planes -> words (swizzled)
+  alignas(16) uint8_t O[17408 + 128];        // payload (bins) | RZE_1^-1 output (subbins)
+  RzeScratch R;
+  uint32_t bad, ticket;
+};
+
 // Copy `len` payload bytes (global, 4-aligned) into shared memory and zero
-// the next 16 bytes.
+// the next 64 bytes.
 __device__ __forceinline__ void load_payload(const uint8_t* g, uint32_t len, uint8_t* s) {
   const uint32_t* g32 = reinterpret_cast<const uint32_t*>(g);
   uint32_t* s32 = reinterpret_cast<uint32_t*>(s);
   for (uint32_t i = threadIdx.x; i < len / 4; i += kCodecThreads) s32[i] = __ldg(&g32[i]);
-  if (threadIdx.x < 4) s32[len / 4 + threadIdx.x] = 0;
+  if (threadIdx.x < 16) s32[len / 4 + threadIdx.x] = 0;
 }
 
 template <typename T>
-__device__ void decode_chunk(const DecodeArgs& a, const Hdr& h, uint32_t c, uint64_t off, uint32_t bsz, uint32_t ssz,
-                             CodecSmem& sm) {
+__device__ __noinline__ void decode_stream(const DecodeArgs& a, const uint8_t* p, uint32_t size, bool subs, DecSmem& sm) {
   using U = typename VT<T>::U;
-  using I = typename VT<T>::I;
   constexpr int K = VT<T>::K;
   constexpr int W = kChunkBytes / K;
   constexpr int PER = W / kCodecThreads;
-  U* WB = reinterpret_cast<U*>(sm.wb);
-  U* WS = reinterpret_cast<U*>(sm.ws);
+  U* WD = reinterpret_cast<U*>(sm.Wd);
   const int tid = threadIdx.x;
-  const uint8_t* pb = a.in + off;
   bool bad = false;
-
-  // bins
-  if (bsz == kChunkBytes) {
-    const U* g = reinterpret_cast<const U*>(pb);
-    for (int i = tid; i < W; i += kCodecThreads) WB[swz(i)] = g[i];
-  } else {
-    load_payload(pb, bsz, sm.ob);
+  PhaseClock pc;
+  pc.start(a.prof);
+  if (size == kChunkBytes) {  // raw words
+    const U* g = reinterpret_cast<const U*>(p);
+    for (int i = tid; i < W; i += kCodecThreads) WD[swz(i)] = g[i];
     __syncthreads();
-    uint32_t used = rze_decode(sm.ob, bsz, kChunkBytes, 1, sm.sh, sm.r);
-    if (used == 0xffffffffu || pad4(used) != bsz) bad = true;
+    pc.mark(a.ctr, subs ? 10 : 9);
+    return;
+  }
+  if (!subs) {
+    load_payload(p, size, sm.O);
+    __syncthreads();
+    const uint32_t used = rze_dec(sm.O, size, kChunkBytes, 1, sm.Wd, sm.R);
+    if (used == 0xffffffffu || pad4(used) != size) bad = true;
+  } else {
+    load_payload(p, size, sm.Wd);
+    __syncthreads();
+    const uint32_t l1 = (uint32_t)sm.Wd[0] | ((uint32_t)sm.Wd[1] << 8);
+    const uint32_t l1max = kChunkBytes + kChunkBytes / K / 8 + 64 + 8;
+    if (l1 > l1max || size < 2) bad = true;
     if (!bad) {
-      bit_inverse<U>(reinterpret_cast<const uint32_t*>(sm.sh), reinterpret_cast<U*>(sm.z), W);
-      __syncthreads();
-      // inverse negabinary + prefix sum (thread owns PER consecutive words)
-      const U* Z = reinterpret_cast<const U*>(sm.z);
-      U d[PER];
-      U run = 0;
-#pragma unroll
-      for (int v = 0; v < PER; ++v) {
-        U u = Z[swz(tid * PER + v)];
-        d[v] = (U)((u ^ nb_mask<U>()) - nb_mask<U>());
-        run += d[v];
-      }
-      U tot;
-      U ex;
-      if constexpr (sizeof(U) == 4)
-        ex = block_scan_excl<uint32_t>(run, sm.r.wsum, &tot);
-      else
-        ex = (U)block_scan_excl<unsigned long long>((unsigned long long)run, sm.r.wsum64,
-                                                     reinterpret_cast<unsigned long long*>(&tot));
-      U acc = ex;
-#pragma unroll
-      for (int v = 0; v < PER; ++v) {
-        acc += d[v];
-        WB[swz(tid * PER + v)] = acc;
-      }
+      const uint32_t used = rze_dec(sm.Wd + 2, size - 2, l1, 1, sm.O, sm.R);
+      if (used == 0xffffffffu || pad4(2 + used) != size) bad = true;
+    }
+    if (!bad) {
+      const uint32_t used2 = rze_dec(sm.O, l1, kChunkBytes, K, sm.Wd, sm.R);
+      if (used2 != l1) bad = true;
     }
   }
-  // subbins
-  const uint8_t* ps = pb + bsz;
-  if (!bad) {
-    if (ssz == kChunkBytes) {
-      const U* g = reinterpret_cast<const U*>(ps);
-      for (int i = tid; i < W; i += kCodecThreads) WS[swz(i)] = g[i];
-    } else {
-      load_payload(ps, ssz, sm.os);
-      __syncthreads();
-      const uint32_t l1 = (uint32_t)sm.os[0] | ((uint32_t)sm.os[1] << 8);
-      const uint32_t l1max = kChunkBytes + kChunkBytes / K / 8 + 64 + 8;
-      if (l1 > l1max) bad = true;
-      if (!bad) {
-        uint32_t used = rze_decode(sm.os + 2, ssz - 2, l1, 1, sm.z, sm.r);
-        if (used == 0xffffffffu || pad4(2 + used) != ssz) bad = true;
-      }
-      if (!bad) {
-        if (tid < 16) sm.z[l1 + tid] = 0;
-        __syncthreads();
-        uint32_t used2 = rze_decode(sm.z, l1, kChunkBytes, K, sm.sh, sm.r);
-        if (used2 != l1) bad = true;
-      }
-      if (!bad) {
-        bit_inverse<U>(reinterpret_cast<const uint32_t*>(sm.sh), WS, W);
-      }
+  pc.mark(a.ctr, subs ? 10 : 9);
+  if (bad) {  // uniform across the block (rze_dec results are block-wide)
+    if (tid == 0) {
+      sm.bad = 1;
+      atomicOr(&a.ctr->err, kErrCorrupt);
     }
-  }
-  if (bad) {
-    if (tid == 0) atomicOr(&a.ctr->err, kErrCorrupt);
     __syncthreads();
     return;
   }
-  __syncthreads();
-  // a8: x^ = value with key(lo(b)) + s, or the raw escape (G10)
+  bit_inverse_inplace<U>(sm.Wd, W);
+  pc.mark(a.ctr, 11);
+  if (!subs) {  // NB^-1 + prefix sum (thread owns PER consecutive words)
+    U d[PER];
+    U run = 0;
+#pragma unroll
+    for (int v = 0; v < PER; ++v) {
+      const U u = WD[swz(tid * PER + v)];
+      d[v] = (U)((u ^ nb_mask<U>()) - nb_mask<U>());
+      run += d[v];
+    }
+    U tot, ex;
+    if constexpr (sizeof(U) == 4)
+      ex = block_scan_excl<uint32_t>(run, sm.R.wsum, &tot);
+    else
+      ex = (U)block_scan_excl<unsigned long long>((unsigned long long)run, sm.R.wsum64,
+                                                   reinterpret_cast<unsigned long long*>(&tot));
+    U acc = ex;
+#pragma unroll
+    for (int v = 0; v < PER; ++v) {
+      acc += d[v];
+      WD[swz(tid * PER + v)] = acc;
+    }
+    __syncthreads();
+    pc.mark(a.ctr, 12);
+  }
+}
+
+// a8: x^ = value with key(lo(b)) + s, or the raw escape (G10), for the
+// half `r` of chunk c; WB/WS point at the two CTAs' word buffers (DSMEM).
+template <typename T>
+__device__ __forceinline__ void reconstruct_half(const DecodeArgs& a, const Hdr& h, uint32_t c, int r, const uint8_t* wb,
+                                                 const uint8_t* ws) {
+  using U = typename VT<T>::U;
+  using I = typename VT<T>::I;
+  constexpr int W = kChunkBytes / VT<T>::K;
+  constexpr int PER = W / kCodecThreads / 2;
+  const U* WB = reinterpret_cast<const U*>(wb);
+  const U* SW = reinterpret_cast<const U*>(ws);
   const uint64_t e0 = (uint64_t)c * W;
   const uint32_t cnt = (uint32_t)min((uint64_t)W, h.n - e0);
   T* O = static_cast<T*>(a.out) + e0;
 #pragma unroll
   for (int v = 0; v < PER; ++v) {
-    const int i = v * kCodecThreads + tid;
+    const int i = (2 * v + r) * kCodecThreads + threadIdx.x;
     if ((uint32_t)i < cnt) {
-      U bw = WB[swz(i)], sw = WS[swz(i)];
+      const U bw = WB[swz(i)], sw = SW[swz(i)];
       U bits;
       if (bw == VT<T>::kSentinel) {
         bits = sw;
       } else {
-        int64_t b = (int64_t)(I)bw;
-        T lo = lo_t<T>(b, h.eps);
-        int64_t k = (int64_t)key_of((U)as_bits(lo)) + (int64_t)sw;
+        const T lo = lo_t<T>((int64_t)(I)bw, h.eps);
+        const int64_t k = (int64_t)key_of((U)as_bits(lo)) + (int64_t)sw;
         if constexpr (sizeof(U) == 4)
           bits = bits_of_key32(k);
         else
           bits = bits_of_key64(k);
       }
       if constexpr (sizeof(U) == 4)
-        O[i] = __uint_as_float(bits);
+        __stcs(&O[i], __uint_as_float(bits));
       else
-        O[i] = __longlong_as_double((long long)bits);
+        __stcs(&O[i], __longlong_as_double((long long)bits));
     }
   }
-  __syncthreads();
 }
 
-__global__ void __launch_bounds__(kCodecThreads, 2) k_decode(DecodeArgs a) {
+__device__ __forceinline__ bool h32_err(const DecodeArgs& a) {
+  return (*(volatile uint32_t*)&a.ctr->err) & (kErrCorrupt | kErrVersion | kErrNoSpace);
+}
+
+// Persistent: each 2-CTA cluster takes chunk tickets until the stream is done.
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kCodecThreads, 4) k_decode(DecodeArgs a) {
+  namespace cg = cooperative_groups;
   extern __shared__ __align__(16) uint8_t smem_raw[];
-  CodecSmem& sm = *reinterpret_cast<CodecSmem*>(smem_raw);
+  DecSmem& sm = *reinterpret_cast<DecSmem*>(smem_raw);
+  cg::cluster_group cl = cg::this_cluster();
   const int tid = threadIdx.x;
+  const int r = (int)cl.block_rank();
+  // every exit below is taken by both CTAs of the cluster (same header, same
+  // flag word, same ticket) so the cluster barriers stay matched
   const Hdr h = parse_header(a);
   if (!h.ok) {
     if (blockIdx.x == 0 && tid == 0) atomicOr(&a.ctr->err, h.err);
     return;
   }
+  if (h32_err(a)) return;  // k_chunk_scan flagged the table
   const uint32_t* tab = reinterpret_cast<const uint32_t*>(a.in + kHdrBytes);
+  const DecSmem* s0 = cl.map_shared_rank(&sm, 0);
+  DecSmem* s1 = cl.map_shared_rank(&sm, 1);
+  if (tid == 0) sm.bad = 0;  // sticky: a corrupt chunk fails the whole call
   for (;;) {
-    if (tid < 32) {
-      uint32_t c = 0;
-      if (tid == 0) c = atomicAdd(&a.ctr->ticket, 1u);
-      c = __shfl_sync(0xffffffffu, c, 0);
-      if (tid == 0) sm.misc[0] = c;
-      if (c < h.C) {
-        const uint32_t bs = tab[2 * c], ss = tab[2 * c + 1];
-        bool ok = bs >= 4 && bs <= kChunkBytes && (bs & 3u) == 0 && ss >= 4 && ss <= kChunkBytes && (ss & 3u) == 0;
-        const uint64_t agg = ok ? (uint64_t)bs + ss : (1ull << 40);  // poison keeps later offsets out of range
-        const uint64_t excl = lookback_warp(a.state, c, agg);
-        const uint64_t off = (uint64_t)kHdrBytes + 8ull * h.C + excl;
-        if (!ok || off + bs + ss > a.in_bytes) ok = false;
-        if (c == h.C - 1 && off + bs + ss != a.in_bytes) ok = false;
-        if (tid == 0) {
-          if (!ok) atomicOr(&a.ctr->err, kErrCorrupt);
-          sm.misc[1] = ok;
-          sm.misc[2] = bs;
-          sm.misc[3] = ss;
-          sm.misc64[0] = off;
-        }
+    if (tid == 0) {
+      if (r == 0) {  // rank 0 draws the ticket and pushes it into both CTAs
+        const uint32_t t = atomicAdd(&a.ctr->ticket, 1u);
+        sm.ticket = t;
+        s1->ticket = t;
       }
     }
-    __syncthreads();
-    const uint32_t c = sm.misc[0];
+    cl.sync();  // ticket visible; the partner finished reading our words
+    const uint32_t c = sm.ticket;  // local copy: the partner may exit after this barrier
     if (c >= h.C) break;
-    if (sm.misc[1]) {
+    const uint32_t sz = tab[2 * c + r];
+    const uint8_t* p = a.in + a.off[c] + (r ? tab[2 * c] : 0u);
+    if (h.dtype == 0)
+      decode_stream<float>(a, p, sz, r != 0, sm);
+    else
+      decode_stream<double>(a, p, sz, r != 0, sm);
+    cl.sync();
+    if (!s0->bad && !s1->bad) {
       if (h.dtype == 0)
-        decode_chunk<float>(a, h, c, sm.misc64[0], sm.misc[2], sm.misc[3], sm);
+        reconstruct_half<float>(a, h, c, r, s0->Wd, s1->Wd);
       else
-        decode_chunk<double>(a, h, c, sm.misc64[0], sm.misc[2], sm.misc[3], sm);
+        reconstruct_half<double>(a, h, c, r, s0->Wd, s1->Wd);
     }
-    __syncthreads();
   }
 }
 

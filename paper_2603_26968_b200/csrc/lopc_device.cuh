@@ -137,6 +137,67 @@ __device__ __forceinline__ bool quantize(T x, double eps, double inv, typename V
   return true;
 }
 
+// f32 data: a float fast path in front of the exact double path.
+// inv32 = RN32(1/eps) (0 disables the fast path; the host sets it only for
+// 2^-120 < eps < 2^120).  t = RN32(x * inv32) differs from x/eps by less than
+// |t| 2^-22; if t is farther than |t| 2^-21 from a half-integer and |t| <
+// 2^22, b = rint(t) is exact.  Otherwise the exact double path decides.
+__device__ __forceinline__ bool quantize_f32(float x, float inv32, double eps, double inv, int32_t& bout) {
+  const float t = __fmul_rn(x, inv32);
+  const float at = fabsf(t);
+  if (at < 4194304.0f) {
+    const float tm = __fadd_rn(t, 12582912.0f);  // 1.5 * 2^23: rint for |t| < 2^22
+    const float r = __fsub_rn(tm, 12582912.0f);
+    const float margin = __fsub_rn(0.5f, __fmul_rn(at, 0x1p-21f));
+    if (fabsf(__fsub_rn(t, r)) < margin) {
+      bout = (int32_t)(__float_as_uint(tm) - __float_as_uint(12582912.0f));
+      return true;
+    }
+  }
+  return quantize<float>(x, eps, inv, bout);
+}
+
+template <typename T>
+__device__ __forceinline__ bool quantize_fast(T x, float inv32, double eps, double inv, typename VT<T>::I& b);
+template <>
+__device__ __forceinline__ bool quantize_fast<float>(float x, float inv32, double eps, double inv, int32_t& b) {
+  return quantize_f32(x, inv32, eps, inv, b);
+}
+template <>
+__device__ __forceinline__ bool quantize_fast<double>(double x, float, double eps, double inv, int64_t& b) {
+  return quantize<double>(x, eps, inv, b);
+}
+
+// Split form of quantize for the codec's bulk loops: qtry_* is the
+// branch-free fast attempt (returns true when it decides b, which then is the
+// exact bin, in range); quantize_slow is the exact path out of line (returns
+// kEscape for an escape).
+constexpr int64_t kEscape = INT64_MIN;
+
+__device__ __forceinline__ bool qtry(float x, float inv32, double, int32_t& b) {
+  const float t = __fmul_rn(x, inv32);
+  const float at = fabsf(t);
+  const float tm = __fadd_rn(t, 12582912.0f);
+  const float r = __fsub_rn(tm, 12582912.0f);
+  const float margin = __fsub_rn(0.5f, __fmul_rn(at, 0x1p-21f));
+  b = (int32_t)(__float_as_uint(tm) - __float_as_uint(12582912.0f));
+  return (at < 4194304.0f) & (fabsf(__fsub_rn(t, r)) < margin);
+}
+__device__ __forceinline__ bool qtry(double x, float, double inv, int64_t& b) {
+  const double t = x * inv;
+  const double at = fabs(t);
+  const double tm = t + kMagic;
+  const double rd = tm - kMagic;
+  const double margin = 0.5 - at * 0x1p-50 - 0x1p-60;
+  b = __double_as_longlong(tm) - __double_as_longlong(kMagic);
+  return (at <= (double)(VT<double>::kBinMax - 1)) & (fabs(t - rd) < margin);
+}
+template <typename T>
+__device__ __noinline__ int64_t quantize_slow(T x, double eps, double inv) {
+  typename VT<T>::I b;
+  return quantize<T>(x, eps, inv, b) ? (int64_t)b : kEscape;
+}
+
 // ---- memory-model helpers ------------------------------------------------
 __device__ __forceinline__ uint64_t ld_acquire_u64(const uint64_t* p) {
   uint64_t v;

@@ -8,11 +8,10 @@
 // here is B200-shaped, not the paper's point worklist:
 //
 //   k_quant_flags   one CTA per 2048-point tile (3D 8x8x32, 2D 64x32) with a
-//                   one-cell halo of value keys in shared memory.  Only the
-//                   tile's own points are quantized: with K_lo(p) =
-//                   key(lo(b_p)), a neighbour n is a same-bin predecessor of p
-//                   iff K_lo(p) <= key(n) < key(p) (+e slots; <= for -e slots,
-//                   the SoS tie rule G4), because bins are key intervals.
+//                   one-cell halo of (value key, exact bin) pairs in shared
+//                   memory; a neighbour n is a same-bin predecessor of p iff
+//                   bin(n) = bin(p) and key(n) < key(p) (+e slots; <= for -e
+//                   slots, the SoS tie rule G4).
 //                   Flags are stored as bit planes: for every 32-point x-row
 //                   segment, word j holds star slot j of its 32 points (one
 //                   warp ballot per slot).
@@ -97,7 +96,8 @@ __host__ __device__ __forceinline__ constexpr int slot_opp(int j) {
 }
 
 struct Counters {
-  uint32_t pad0[3];
+  uint32_t ticket2;  // k_chunk_scan tiles
+  uint32_t pad0[2];
   uint32_t ticket;
   uint32_t err;  // kErr* bits
   uint32_t max_s;
@@ -112,6 +112,25 @@ struct Counters {
   unsigned long long raised;
   unsigned long long list_count[3];  // point worklists (rotating)
   uint32_t pass_items[kPassHist];    // [1] tiles of the dense pass, [q>1] worklist points of pass q
+  unsigned long long phase[16];      // diagnostic: SM cycles per codec phase (lopc_set_timing(2))
+};
+
+// Diagnostic phase clock: thread 0 of a block adds the cycles since the last
+// mark to ctr->phase[i] (only when enabled; all threads are past a barrier).
+struct PhaseClock {
+  long long t;
+  bool on;
+  __device__ __forceinline__ void start(bool enable) {
+    on = enable && threadIdx.x == 0;
+    if (on) t = clock64();
+  }
+  __device__ __forceinline__ void mark(Counters* c, int i) {
+    if (on) {
+      const long long n = clock64();
+      atomicAdd(&c->phase[i], (unsigned long long)(n - t));
+      t = n;
+    }
+  }
 };
 
 enum : uint32_t {
@@ -133,6 +152,7 @@ struct RepairArgs {
   uint64_t bmw;       // words per bitmap
   Counters* ctr;
   double eps, inv;
+  float inv32;         // RN32(1/eps) for the f32 fast path, NaN = off
   int64_t d0, d1, d2;  // z, y, x extents (2D: d0 = 1)
   int64_t nseg;        // 32-point segments per x-row
   int ntz, nty, ntx;
@@ -220,10 +240,15 @@ __device__ __forceinline__ bool tile_interior(Idx z0, Idx y0, Idx x0, Idx d0, Id
 // ---------------------------------------------------------------------------
 // k_quant_flags: a1 (exact bins of the tile's points) + a2 (flags).
 // ---------------------------------------------------------------------------
+template <typename T>
+struct KeyBin {
+  typename VT<T>::I key, bin;
+};
+
 template <typename T, int NDIM>
 constexpr size_t quant_flags_smem() {
   using G = Geo<NDIM>;
-  return (size_t)G::HZ * G::HY * G::HX * sizeof(typename VT<T>::I) + 16;
+  return (size_t)G::HZ * G::HY * G::HX * sizeof(KeyBin<T>) + 16;
 }
 
 template <typename T, int NDIM, typename Idx>
@@ -235,10 +260,10 @@ __global__ void __launch_bounds__(kRepairThreads, 3) k_quant_flags(RepairArgs a)
   constexpr int TP = G::TZ * G::TY * G::TX;
   constexpr int PPT = TP / kRepairThreads;
   constexpr int D = G::D;
-  constexpr I kOut = (I)VT<T>::kSentinel;  // below every key: outside the grid
+  constexpr I kOut = (I)VT<T>::kSentinel;  // below every key: outside the grid; also "no bin"
 
   extern __shared__ __align__(16) uint8_t qf_smem[];
-  I* skey = reinterpret_cast<I*>(qf_smem);
+  KeyBin<T>* kb = reinterpret_cast<KeyBin<T>*>(qf_smem);
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int tx = blockIdx.x, ty = blockIdx.y, tz = blockIdx.z;  // 3D launch grid: no index division
@@ -246,6 +271,7 @@ __global__ void __launch_bounds__(kRepairThreads, 3) k_quant_flags(RepairArgs a)
   const Idx z0 = (Idx)tz * G::TZ, y0 = (Idx)ty * G::TY, x0 = (Idx)tx * G::TX;
   const bool interior = tile_interior<NDIM, Idx>(z0, y0, x0, d0, d1, d2);
 
+  // halo: value key and exact bin (a1) of every point of tile + halo
   {
     HaloLoad<NDIM, U, Idx> L;
     L.load(static_cast<const U*>(a.x), z0, y0, x0, d0, d1, d2, interior, (U)0);
@@ -255,30 +281,38 @@ __global__ void __launch_bounds__(kRepairThreads, 3) k_quant_flags(RepairArgs a)
 #pragma unroll
       for (int e = 0; e < HR::EPL; ++e) {
         const int hx = lane + 32 * e;
-        if (r < HR::R && hx < G::HX) skey[r * G::HX + hx] = L.ok[i][e] ? (I)key_of(L.v[i][e]) : kOut;
+        if (r < HR::R && hx < G::HX) {
+          KeyBin<T> v{kOut, kOut};
+          if (L.ok[i][e]) {
+            v.key = (I)key_of(L.v[i][e]);
+            I b;
+            if (quantize_fast<T>(value_of_key<T>(v.key), a.inv32, a.eps, a.inv, b)) v.bin = b;
+          }
+          kb[r * G::HX + hx] = v;
+        }
       }
     }
   }
   __syncthreads();
 
-  // Warp w, step k handles tile row (w + 16k): lane = x.  Flags leave as one
-  // ballot per slot (bit plane), written by lane j as word j of the segment.
+  // a2 (Alg. 1 loop 2): warp w, step k handles tile row (w + 16k): lane = x.
+  // Flags leave as one ballot per slot (bit plane), written by lane j as word
+  // j of the row's 32-point segment.
 #pragma unroll
   for (int k = 0; k < PPT; ++k) {
     const int row = warp + k * (kRepairThreads / 32);
     const int lz = row / G::TY, ly = row % G::TY;
     const int h = ((lz + G::ZH) * G::HY + (ly + 1)) * G::HX + (lane + 1);
-    const I kp = skey[h];
+    const KeyBin<T> p = kb[h];
     uint32_t m = 0;
-    I b;
-    if (kp != kOut && quantize<T>(value_of_key<T>(kp), a.eps, a.inv, b)) {
-      const I kl = (I)key_of((U)as_bits(lo_t<T>((int64_t)b, a.eps)));
+    if (p.bin != kOut) {
 #pragma unroll
       for (int j = 0; j < 2 * D; ++j) {
-        const I kn = skey[h + slot_hoff<NDIM>(j)];
-        // n precedes p in SoS order within p's bin: bins are key intervals, so
-        // K_lo(p) <= key(n) < key(p) (+e slots) or <= key(p) (-e slots, G4)
-        const bool arc = kn >= kl && (j < D ? kn < kp : kn <= kp);
+        const KeyBin<T> q = kb[h + slot_hoff<NDIM>(j)];
+        // n is a same-bin predecessor of p: same bin and n precedes p in the
+        // SoS order (a +e neighbour has the larger index, so only a smaller
+        // key; a -e neighbour also wins ties, G4)
+        const bool arc = q.bin == p.bin && (j < D ? q.key < p.key : q.key <= p.key);
         m |= (uint32_t)arc << j;
       }
     }

@@ -36,7 +36,7 @@ class Stats(C.Structure):
                                           "inner_iters", "escapes", "bin_bytes", "sub_bytes", "total_bytes")] + [
         ("max_subbin", C.c_uint32), ("timing_valid", C.c_uint32)] + [
         (n, C.c_float) for n in ("ms_h2d", "ms_quant_repair", "ms_sweep", "ms_encode", "ms_decode", "ms_d2h",
-                                 "ms_total")] + [("raised", C.c_uint64), ("pass_items", C.c_uint32 * 16)]
+                                 "ms_total")] + [("raised", C.c_uint64), ("pass_items", C.c_uint32 * 16), ("phase_cycles", C.c_uint64 * 16)]
 
 
 _lib = None
@@ -199,8 +199,8 @@ def repair(x: torch.Tensor, eps: float):
     return flags, s
 
 
-def set_timing(on: bool = True):
-    load(False).lopc_set_timing(1 if on else 0)
+def set_timing(on=True):
+    load(False).lopc_set_timing(int(on) if not isinstance(on, bool) else (1 if on else 0))
 
 
 def last_stats() -> dict:
@@ -208,4 +208,5 @@ def last_stats() -> dict:
     load(False).lopc_last_stats(C.byref(st))
     d = {name: getattr(st, name) for name, _ in Stats._fields_}
     d["pass_items"] = [int(v) for v in st.pass_items]
+    d["phase_cycles"] = [int(v) for v in st.phase_cycles]
     return d

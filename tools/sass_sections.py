@@ -6,7 +6,7 @@ import sys
 
 rows = list(csv.reader(open(sys.argv[1])))
 hdr = rows[1]
-data = rows[2:]
+data = [r for r in rows[2:] if len(r) == len(hdr) and r[0].startswith("0x")]
 ii = hdr.index("Instructions Executed")
 src = hdr.index("Source")
 si = hdr.index("Warp Stall Sampling (All Samples)")
