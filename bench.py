@@ -51,50 +51,56 @@ def load_peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+    """SM clocks and throttle reasons sampled DURING the timed region through
+    NVML (a background thread polling every ~2 ms), so that even a short timed
+    region gets samples."""
+
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+               "hw_power_brake_slowdown": 0x80, "sw_power_cap": 0x4}
 
     def __init__(self, index: int):
         self.index = index
         self.samples = []
-        self.proc = None
+        self.stop = threading.Event()
+        self.t = None
+        self.err = None
+
+    def _run(self):
+        try:
+            import pynvml as nv
+
+            nv.nvmlInit()
+            h = nv.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+            self.ready.set()
+            while not self.stop.is_set():
+                sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                self.samples.append((sm, r))
+                time.sleep(0.002)
+        except Exception as e:  # no NVML: reported as unsampled
+            self.err = repr(e)
+            self.ready.set()
 
     def __enter__(self):
-        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
-             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-             "clocks_event_reasons.sw_power_cap")
-        try:
-            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
-                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
-            self.t.start()
-        except OSError:
-            self.proc = None
+        self.ready = threading.Event()
+        self.t = threading.Thread(target=self._run, daemon=True)
+        self.t.start()
+        self.ready.wait(10)
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            parts = [p.strip() for p in line.split(",")]
-            if len(parts) >= 7:
-                self.samples.append(parts)
-
     def __exit__(self, *a):
-        if self.proc:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except subprocess.TimeoutExpired:
-                self.proc.kill()
+        self.stop.set()
+        if self.t:
+            self.t.join(5)
 
     def summary(self):
         if not self.samples:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[3 + i].lower() == "active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.samples)}
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "error": self.err}
+        sm = [v for v, _ in self.samples]
+        reasons = sorted({n for _, r in self.samples for n, bit in self.REASONS.items() if r & bit})
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": getattr(self, "max_mhz", None),
+                "reasons": reasons, "samples": len(self.samples), "source": "nvml, 2 ms polling"}
 
 
 def cpu_model():
@@ -210,8 +216,9 @@ def main():
     nbytes_stream = int(st.numel())
 
     lopc.set_timing(True)
-    comp_ms, dec_ms, kern = [], [], {"quant_repair": [], "sweep": [], "encode": [], "decode": []}
-    passes, tiles = [], []
+    comp_ms, dec_ms = [], []
+    kern = {k: [] for k in ("quant_flags", "sweep", "encode", "place", "decode_scan", "decode")}
+    tiles, launches = [], 0
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
     if dist:
         dist.barrier()
@@ -229,11 +236,13 @@ def main():
             torch.cuda.synchronize()
             comp_ms.append(ev[0].elapsed_time(ev[1]))
             dec_ms.append(ev[1].elapsed_time(ev[2]))
-            kern["quant_repair"].append(sc["ms_quant_repair"])
+            kern["quant_flags"].append(sc["ms_quant_repair"])
             kern["sweep"].append(sc["ms_sweep"])
             kern["encode"].append(sc["ms_encode"])
+            kern["place"].append(sc["ms_place"])
+            kern["decode_scan"].append(sd["ms_place"])
             kern["decode"].append(sd["ms_decode"])
-            passes.append(sc["sweep_passes"])
+            launches += sc["launches"] + sd["launches"]
             tiles.append(sc["worklist_points"])
             rep = {k: sc[k] for k in ("sweep_passes", "worklist_points", "inner_iters", "raised", "max_subbin",
                                       "escapes", "n_tiles", "bin_bytes", "sub_bytes")}
@@ -278,22 +287,20 @@ def main():
         return
 
     # ---- roofline of the dominant kernel ----------------------------------
+    # algorithmic bytes per launch: x is k bytes/point, the
+    # bit-plane flags F = 2 (3D) / 1 (2D) bytes/point, s is u32.
     peak, peak_src = load_peaks()
     n = x_np.size
     k = x_np.itemsize
     F = 2 if x_np.ndim == 3 else 1
     med = {kk: statistics.median(v) for kk, v in kern.items()}
-    tiles_pts = 2048
     alg = {
-        # read x, write flags + s
-        "quant_repair": n * (k + F + 4),
-        # dense pass: read flags, write s; sparse passes: per worklist point
-        # read flags + s (neighbour re-reads are served by L2, not counted)
-        "sweep": n * (F + 4) + statistics.median(tiles) * (F + 4),
-        # read x + s, write the stream
-        "encode": n * (k + 4) + nbytes_stream,
-        # read the stream, write x^
-        "decode": nbytes_stream + n * k,
+        "quant_flags": n * (k + F),                                        # read x, write flags
+        "sweep": n * (F + 4) + statistics.median(tiles) * (F + 4),         # dense: flags -> s; sparse: per point
+        "encode": n * (k + 4) + nbytes_stream,                             # read x + s, write payloads
+        "place": 2 * nbytes_stream,                                        # staged payloads -> stream
+        "decode_scan": 16 * ((n * k + 16383) // 16384),                   # size table in, offsets out
+        "decode": nbytes_stream + n * k,                                   # read stream, write x^
     }
     dom = max(med, key=lambda kk: med[kk])
     achieved = alg[dom] / (med[dom] / 1e3) / 1e9 if med[dom] > 0 else 0.0
@@ -323,12 +330,13 @@ def main():
         "repair": rep,
         "per_kernel": per_kernel,
         "roofline": {"kernel": f"k_{dom}", "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src},
+                     "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                     "alg_bytes_per_launch": alg[dom], "launch_ms": med[dom]},
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_val, "unit": "GB/s", "h2d_bytes_per_step": raw + nbytes_stream,
                 "d2h_bytes_per_step": nbytes_stream + raw,
                 "note": "lopc_compress/lopc_decompress on pinned host buffers, staging copies inside the call"},
-        "gpu_launches": 4 * K,
+        "gpu_launches": launches,
         "clocks": clk.summary(),
     }
     print(json.dumps(line), flush=True)

@@ -118,6 +118,8 @@ typedef struct {
   uint64_t raised;            /* subbins raised above 0 (dense pass) or raised again (sparse passes) */
   uint32_t pass_items[16];    /* [1]: tiles of the dense pass; [q>1]: worklist points of pass q */
   uint64_t phase_cycles[16];  /* diagnostic (lopc_set_timing(2)): SM cycles per codec phase, summed over chunks */
+  float ms_place;             /* compress: k_chunk_scan + k_place; decompress: k_chunk_scan */
+  uint32_t launches;          /* kernels this library launched in the call */
 } lopc_stats;
 
 int lopc_last_stats(lopc_stats* out);

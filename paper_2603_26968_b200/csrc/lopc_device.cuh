@@ -25,6 +25,8 @@ struct VT<float> {
   using I = int32_t;   // bin and ord
   static constexpr int K = 4;
   static constexpr U kSentinel = 0x80000000u;
+  static constexpr U kSignBit = 0x80000000u;
+  static constexpr U kInfBits = 0x7f800000u;
   static constexpr double kBinMax = 2147483646.0;
 };
 template <>
@@ -33,6 +35,8 @@ struct VT<double> {
   using I = int64_t;
   static constexpr int K = 8;
   static constexpr U kSentinel = 0x8000000000000000ull;
+  static constexpr U kSignBit = 0x8000000000000000ull;
+  static constexpr U kInfBits = 0x7ff0000000000000ull;
   static constexpr double kBinMax = 1125899906842624.0;
 };
 

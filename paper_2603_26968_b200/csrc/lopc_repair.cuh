@@ -158,6 +158,8 @@ struct RepairArgs {
   int ntz, nty, ntx;
   int64_t ntiles;
   int max_passes;
+  int64_t own_lo, own_hi;  // points with incoming arcs: [own_lo, own_hi) (slab mode; else [0, N))
+  int skip_dense;          // k_sweep: start with the sparse passes (slab rounds >= 2)
 };
 
 // Enqueue point q for pass `pass` (dedup by the pass's bitmap).
@@ -239,16 +241,21 @@ __device__ __forceinline__ bool tile_interior(Idx z0, Idx y0, Idx x0, Idx d0, Id
 
 // ---------------------------------------------------------------------------
 // k_quant_flags: a1 (exact bins of the tile's points) + a2 (flags).
+//
+// Same-bin test without the neighbour's bin: keys (ord) are monotone in x and
+// bins are key intervals [key(lo(b)), key(lo(b+1))), so for a regular p with
+// bin b_p and any neighbour n,
+//   n ~> p  <=>  key(lo(b_p)) <= key_n < key_p        (+e slot: n has larger idx)
+//   n ~> p  <=>  key(lo(b_p)) <= key_n <= key_p       (-e slot: n wins ties, G4)
+// (key_n in [lo(b_p), x_p] puts n in bin b_p, hence regular; NaN and
+// out-of-grid neighbours carry a key below every lo key; an escaped p gets
+// lo key = max, so it has no incoming arcs, O8).  Halo points therefore need
+// only their key; only the tile's own points are quantized.
 // ---------------------------------------------------------------------------
-template <typename T>
-struct KeyBin {
-  typename VT<T>::I key, bin;
-};
-
 template <typename T, int NDIM>
 constexpr size_t quant_flags_smem() {
   using G = Geo<NDIM>;
-  return (size_t)G::HZ * G::HY * G::HX * sizeof(KeyBin<T>) + 16;
+  return (size_t)G::HZ * G::HY * G::HX * sizeof(typename VT<T>::I) + 16;
 }
 
 template <typename T, int NDIM, typename Idx>
@@ -260,10 +267,11 @@ __global__ void __launch_bounds__(kRepairThreads, 3) k_quant_flags(RepairArgs a)
   constexpr int TP = G::TZ * G::TY * G::TX;
   constexpr int PPT = TP / kRepairThreads;
   constexpr int D = G::D;
-  constexpr I kOut = (I)VT<T>::kSentinel;  // below every key: outside the grid; also "no bin"
+  constexpr I kLow = (I)VT<T>::kSentinel;                                    // NaN / outside the grid
+  constexpr I kHigh = (I)(((typename std::make_unsigned<I>::type)kLow) - 1u);  // max: escaped p
 
   extern __shared__ __align__(16) uint8_t qf_smem[];
-  KeyBin<T>* kb = reinterpret_cast<KeyBin<T>*>(qf_smem);
+  I* K = reinterpret_cast<I*>(qf_smem);
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int tx = blockIdx.x, ty = blockIdx.y, tz = blockIdx.z;  // 3D launch grid: no index division
@@ -271,7 +279,7 @@ __global__ void __launch_bounds__(kRepairThreads, 3) k_quant_flags(RepairArgs a)
   const Idx z0 = (Idx)tz * G::TZ, y0 = (Idx)ty * G::TY, x0 = (Idx)tx * G::TX;
   const bool interior = tile_interior<NDIM, Idx>(z0, y0, x0, d0, d1, d2);
 
-  // halo: value key and exact bin (a1) of every point of tile + halo
+  // halo: keys only
   {
     HaloLoad<NDIM, U, Idx> L;
     L.load(static_cast<const U*>(a.x), z0, y0, x0, d0, d1, d2, interior, (U)0);
@@ -282,20 +290,16 @@ __global__ void __launch_bounds__(kRepairThreads, 3) k_quant_flags(RepairArgs a)
       for (int e = 0; e < HR::EPL; ++e) {
         const int hx = lane + 32 * e;
         if (r < HR::R && hx < G::HX) {
-          KeyBin<T> v{kOut, kOut};
-          if (L.ok[i][e]) {
-            v.key = (I)key_of(L.v[i][e]);
-            I b;
-            if (quantize_fast<T>(value_of_key<T>(v.key), a.inv32, a.eps, a.inv, b)) v.bin = b;
-          }
-          kb[r * G::HX + hx] = v;
+          const U u = L.v[i][e];
+          const bool nan = (u & ~VT<T>::kSignBit) > VT<T>::kInfBits;
+          K[r * G::HX + hx] = (L.ok[i][e] && !nan) ? (I)key_of(u) : kLow;
         }
       }
     }
   }
   __syncthreads();
 
-  // a2 (Alg. 1 loop 2): warp w, step k handles tile row (w + 16k): lane = x.
+  // a1 + a2 (Alg. 1 loop 2): warp w, step k handles tile row (w + 16k): lane = x.
   // Flags leave as one ballot per slot (bit plane), written by lane j as word
   // j of the row's 32-point segment.
 #pragma unroll
@@ -303,28 +307,31 @@ __global__ void __launch_bounds__(kRepairThreads, 3) k_quant_flags(RepairArgs a)
     const int row = warp + k * (kRepairThreads / 32);
     const int lz = row / G::TY, ly = row % G::TY;
     const int h = ((lz + G::ZH) * G::HY + (ly + 1)) * G::HX + (lane + 1);
-    const KeyBin<T> p = kb[h];
-    uint32_t m = 0;
-    if (p.bin != kOut) {
-#pragma unroll
-      for (int j = 0; j < 2 * D; ++j) {
-        const KeyBin<T> q = kb[h + slot_hoff<NDIM>(j)];
-        // n is a same-bin predecessor of p: same bin and n precedes p in the
-        // SoS order (a +e neighbour has the larger index, so only a smaller
-        // key; a -e neighbour also wins ties, G4)
-        const bool arc = q.bin == p.bin && (j < D ? q.key < p.key : q.key <= p.key);
-        m |= (uint32_t)arc << j;
-      }
+    const I kp = K[h];
+    I lok = kHigh;
+    if (kp != kLow) {
+      const T xp = value_of_key<T>(kp);
+      I b;
+      if (quantize_fast<T>(xp, a.inv32, a.eps, a.inv, b)) lok = (I)key_of((U)as_bits(lo_t<T>((int64_t)b, a.eps)));
     }
     uint32_t word = 0;
 #pragma unroll
     for (int j = 0; j < 2 * D; ++j) {
-      const uint32_t bj = __ballot_sync(0xffffffffu, (m >> j) & 1u);
+      const I kn = K[h + slot_hoff<NDIM>(j)];
+      const bool arc = kn >= lok && (j < D ? kn < kp : kn <= kp);
+      const uint32_t bj = __ballot_sync(0xffffffffu, arc);
       if (lane == j) word = bj;
     }
     const Idx gz = z0 + lz, gy = y0 + ly;
-    if (lane < G::SW && gz < d0 && gy < d1)
-      a.flags[((size_t)(gz * d1 + gy) * (size_t)a.nseg + (size_t)tx) * G::SW + lane] = word;
+    if (lane < G::SW && gz < d0 && gy < d1) {
+      // slab mode: points outside the owned range get no incoming arcs
+      const Idx rb = (gz * d1 + gy) * d2 + x0;
+      const Idx lo_rel = (Idx)a.own_lo - rb, hi_rel = (Idx)a.own_hi - rb;
+      uint32_t own = 0xffffffffu;
+      if (lo_rel > 0) own = lo_rel >= 32 ? 0u : own << (uint32_t)lo_rel;
+      if (hi_rel < 32) own &= hi_rel <= 0 ? 0u : (0xffffffffu >> (uint32_t)(32 - hi_rel));
+      a.flags[((size_t)(gz * d1 + gy) * (size_t)a.nseg + (size_t)tx) * G::SW + lane] = word & own;
+    }
   }
 }
 
@@ -402,7 +409,7 @@ __global__ void __launch_bounds__(kSweepThreads, 3) k_sweep(RepairArgs a) {
 
   // ---- pass 1: dense, one warp per tile, bit-parallel levels -----------------
   const uint32_t gwarp = blockIdx.x * kSweepWarps + warp, nwarps = gridDim.x * kSweepWarps;
-  for (uint32_t tile = gwarp; tile < (uint32_t)a.ntiles; tile += nwarps) {
+  for (uint32_t tile = gwarp; tile < (a.skip_dense ? 0u : (uint32_t)a.ntiles); tile += nwarps) {
     const uint32_t tz = tile / ntxy, rem = tile - tz * ntxy;
     const uint32_t ty = rem / ntx, tx = rem - ty * ntx;
     const Idx z0 = (Idx)tz * G::TZ, y0 = (Idx)ty * G::TY, x0 = (Idx)tx * G::TX;
@@ -555,7 +562,7 @@ __global__ void __launch_bounds__(kSweepThreads, 3) k_sweep(RepairArgs a) {
       }
     }
   }
-  if (tid == 0 && blockIdx.x == 0) a.ctr->pass_items[1] = (uint32_t)a.ntiles;
+  if (tid == 0 && blockIdx.x == 0 && !a.skip_dense) a.ctr->pass_items[1] = (uint32_t)a.ntiles;
   grid.sync();
 
   // ---- passes >= 2: sparse, point-level ------------------------------------
