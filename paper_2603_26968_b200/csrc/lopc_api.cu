@@ -189,8 +189,12 @@ int host_ctr(Counters*& h) {
   return LOPC_OK;
 }
 
+// Per-call CUDA-event marks (lopc_set_timing).  The events are created once
+// per device and reused, so timing adds no allocation to the call.
+cudaEvent_t g_ev[8] = {};
+int g_ev_dev = -1;
 struct Timer {
-  cudaEvent_t ev[8] = {};
+  cudaEvent_t* ev = g_ev;
   int n = 0;
   bool on = false;
   cudaStream_t st = nullptr;
@@ -198,7 +202,12 @@ struct Timer {
     st = s;
     on = g_timing != 0;
     if (!on) return LOPC_OK;
-    for (int i = 0; i < 8; ++i) CK(cudaEventCreate(&ev[i]));
+    int dev;
+    CK(cudaGetDevice(&dev));
+    if (g_ev_dev != dev) {
+      for (int i = 0; i < 8; ++i) CK(cudaEventCreate(&g_ev[i]));
+      g_ev_dev = dev;
+    }
     return LOPC_OK;
   }
   void mark() {
@@ -208,11 +217,6 @@ struct Timer {
     float v = 0;
     if (on && b < n) cudaEventElapsedTime(&v, ev[a], ev[b]);
     return v;
-  }
-  ~Timer() {
-    if (on)
-      for (int i = 0; i < 8; ++i)
-        if (ev[i]) cudaEventDestroy(ev[i]);
   }
 };
 
@@ -272,6 +276,7 @@ int run_repair(const Shape& sh, const void* x, double eps, uint8_t* ws, const CL
   ra.own_lo = 0;
   ra.own_hi = (int64_t)sh.n;
   ra.skip_dense = 0;
+  ra.prof = g_timing >= 2;
   const dim3 tgrid((unsigned)L.ntx, (unsigned)L.nty, (unsigned)L.ntz);
   const bool i32 = sh.n < (1ull << 31) - (1ull << 24);
   int occ = sh.ndims == 3 ? (i32 ? di->occ_sweep3 : di->occ_sweep3w) : (i32 ? di->occ_sweep2 : di->occ_sweep2w);

@@ -68,6 +68,7 @@ constexpr int kSweepThreads = 256;
 constexpr int kSweepWarps = kSweepThreads / 32;
 constexpr int kPassHist = 16;
 constexpr int kLevelPlanes = 8;  // dense-pass levels per tile before handing over to the worklist
+constexpr unsigned long long kSmallList = 256;  // sparse passes this short run on one block
 constexpr int kMaxLevel = (1 << kLevelPlanes) - 1;
 
 // Star slot j (G2): j < D is +e, j >= D is -e, with e = (j mod D) + 1 read
@@ -97,7 +98,8 @@ __host__ __device__ __forceinline__ constexpr int slot_opp(int j) {
 
 struct Counters {
   uint32_t ticket2;  // k_chunk_scan tiles
-  uint32_t pad0[2];
+  uint32_t tile_ticket;  // k_sweep dense pass: dynamic tile assignment
+  uint32_t pad0;
   uint32_t ticket;
   uint32_t err;  // kErr* bits
   uint32_t max_s;
@@ -160,18 +162,34 @@ struct RepairArgs {
   int max_passes;
   int64_t own_lo, own_hi;  // points with incoming arcs: [own_lo, own_hi) (slab mode; else [0, N))
   int skip_dense;          // k_sweep: start with the sparse passes (slab rounds >= 2)
+  int prof;                // diagnostic: k_sweep pass times (ns) into ctr->phase[14..15]
 };
 
-// Enqueue point q for pass `pass` (dedup by the pass's bitmap).
+__device__ __forceinline__ uint64_t gtimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Enqueue point q for pass `pass` if `valid` (dedup by the pass's bitmap).
+// Warp-collective (all 32 lanes call it together): one list-counter atomic
+// per warp instead of one per point.
 template <typename Idx>
-__device__ __forceinline__ void enqueue(const RepairArgs& a, Idx q, int pass) {
+__device__ __forceinline__ void enqueue_warp(const RepairArgs& a, Idx q, bool valid, int pass) {
   using UIdx = typename std::make_unsigned<Idx>::type;
-  const uint32_t bit = 1u << ((uint32_t)q & 31u);
-  const uint32_t old = atomicOr(&a.bitmap[(size_t)(pass & 1) * a.bmw + ((UIdx)q >> 5)], bit);
-  if (!(old & bit)) {
-    const unsigned long long slot = atomicAdd(&a.ctr->list_count[pass % 3], 1ull);
-    static_cast<UIdx*>(a.plist)[(size_t)(pass & 1) * a.cap + slot] = (UIdx)q;
+  bool fresh = false;
+  if (valid) {
+    const uint32_t bit = 1u << ((uint32_t)q & 31u);
+    const uint32_t old = atomicOr(&a.bitmap[(size_t)(pass & 1) * a.bmw + ((UIdx)q >> 5)], bit);
+    fresh = !(old & bit);
   }
+  const uint32_t m = __ballot_sync(0xffffffffu, fresh);
+  if (!m) return;
+  const int lane = threadIdx.x & 31;
+  unsigned long long base = 0;
+  if (lane == 0) base = atomicAdd(&a.ctr->list_count[pass % 3], (unsigned long long)__popc(m));
+  base = __shfl_sync(0xffffffffu, base, 0);
+  if (fresh) static_cast<UIdx*>(a.plist)[(size_t)(pass & 1) * a.cap + base + __popc(m & ((1u << lane) - 1u))] = (UIdx)q;
 }
 
 // Rows of the halo box handled per warp, and elements per lane per row.
@@ -314,23 +332,30 @@ __global__ void __launch_bounds__(kRepairThreads, 3) k_quant_flags(RepairArgs a)
       I b;
       if (quantize_fast<T>(xp, a.inv32, a.eps, a.inv, b)) lok = (I)key_of((U)as_bits(lo_t<T>((int64_t)b, a.eps)));
     }
-    uint32_t word = 0;
+    uint32_t wv[G::SW];  // the ballots are warp-uniform: lane 0 stores the segment
+#pragma unroll
+    for (int j = 0; j < G::SW; ++j) wv[j] = 0;
 #pragma unroll
     for (int j = 0; j < 2 * D; ++j) {
       const I kn = K[h + slot_hoff<NDIM>(j)];
       const bool arc = kn >= lok && (j < D ? kn < kp : kn <= kp);
-      const uint32_t bj = __ballot_sync(0xffffffffu, arc);
-      if (lane == j) word = bj;
+      wv[j] = __ballot_sync(0xffffffffu, arc);
     }
     const Idx gz = z0 + lz, gy = y0 + ly;
-    if (lane < G::SW && gz < d0 && gy < d1) {
-      // slab mode: points outside the owned range get no incoming arcs
+    if (lane == 0 && gz < d0 && gy < d1) {
       const Idx rb = (gz * d1 + gy) * d2 + x0;
-      const Idx lo_rel = (Idx)a.own_lo - rb, hi_rel = (Idx)a.own_hi - rb;
-      uint32_t own = 0xffffffffu;
-      if (lo_rel > 0) own = lo_rel >= 32 ? 0u : own << (uint32_t)lo_rel;
-      if (hi_rel < 32) own &= hi_rel <= 0 ? 0u : (0xffffffffu >> (uint32_t)(32 - hi_rel));
-      a.flags[((size_t)(gz * d1 + gy) * (size_t)a.nseg + (size_t)tx) * G::SW + lane] = word & own;
+      if (rb < (Idx)a.own_lo || rb + 32 > (Idx)a.own_hi) {
+        // slab mode: points outside the owned range get no incoming arcs
+        const Idx lo_rel = (Idx)a.own_lo - rb, hi_rel = (Idx)a.own_hi - rb;
+        uint32_t own = 0xffffffffu;
+        if (lo_rel > 0) own = lo_rel >= 32 ? 0u : own << (uint32_t)lo_rel;
+        if (hi_rel < 32) own &= hi_rel <= 0 ? 0u : (0xffffffffu >> (uint32_t)(32 - hi_rel));
+#pragma unroll
+        for (int j = 0; j < G::SW; ++j) wv[j] &= own;
+      }
+      uint4* dst = reinterpret_cast<uint4*>(a.flags + ((size_t)(gz * d1 + gy) * (size_t)a.nseg + (size_t)tx) * G::SW);
+#pragma unroll
+      for (int q = 0; q < G::SW / 4; ++q) dst[q] = make_uint4(wv[4 * q], wv[4 * q + 1], wv[4 * q + 2], wv[4 * q + 3]);
     }
   }
 }
@@ -407,9 +432,14 @@ __global__ void __launch_bounds__(kSweepThreads, 3) k_sweep(RepairArgs a) {
   const size_t nseg = (size_t)a.nseg;
   const uint32_t ntx = (uint32_t)a.ntx, ntxy = (uint32_t)a.ntx * (uint32_t)a.nty;
 
+  const uint64_t t_start = (a.prof && tid == 0 && blockIdx.x == 0) ? gtimer() : 0;
   // ---- pass 1: dense, one warp per tile, bit-parallel levels -----------------
   const uint32_t gwarp = blockIdx.x * kSweepWarps + warp, nwarps = gridDim.x * kSweepWarps;
-  for (uint32_t tile = gwarp; tile < (a.skip_dense ? 0u : (uint32_t)a.ntiles); tile += nwarps) {
+  const uint32_t ntl = a.skip_dense ? 0u : (uint32_t)a.ntiles;
+  uint32_t tile = 0;
+  if (lane == 0) tile = atomicAdd(&a.ctr->tile_ticket, 1u);
+  tile = __shfl_sync(0xffffffffu, tile, 0);
+  for (; tile < ntl;) {
     const uint32_t tz = tile / ntxy, rem = tile - tz * ntxy;
     const uint32_t ty = rem / ntx, tx = rem - ty * ntx;
     const Idx z0 = (Idx)tz * G::TZ, y0 = (Idx)ty * G::TY, x0 = (Idx)tx * G::TX;
@@ -524,81 +554,110 @@ __global__ void __launch_bounds__(kSweepThreads, 3) k_sweep(RepairArgs a) {
       if (gz < d0 && gy < d1 && gx < d2) __stcg(&a.s[(gz * d1 + gy) * d2 + gx], sv);
     }
     // border points with s > 0 feed out-of-tile points that assumed s = 0
+    // (all lanes stay converged: the enqueues are warp-collective)
 #pragma unroll
     for (int i = 0; i < 2; ++i) {
-      const uint32_t lv = lev1[i] & vmask;
+      const uint32_t lv = rin[i] ? lev1[i] & vmask : 0u;
       my_raised += __popc(lv);
-      if (!rin[i]) continue;
       if (capped) {  // unfinished: continue point-wise from the top level
-        uint32_t c = X[i] & vmask;
-        while (c) {
-          const int x = __ffs(c) - 1;
+        uint32_t c = rin[i] ? X[i] & vmask : 0u;
+        while (__any_sync(0xffffffffu, c != 0)) {
+          const int x = c ? __ffs(c) - 1 : 0;
+          enqueue_warp<Idx>(a, ((z0 + lz[i]) * d1 + (y0 + ly[i])) * d2 + x0 + x, c != 0, 2);
           c &= c - 1;
-          enqueue<Idx>(a, ((z0 + lz[i]) * d1 + (y0 + ly[i])) * d2 + x0 + x, 2);
         }
       }
-      if (!lv) continue;
-#pragma unroll
+      if (!__any_sync(0xffffffffu, lv != 0)) continue;
+#pragma unroll 1
       for (int j = 0; j < 2 * D; ++j) {
         const int dz = slot_dz<NDIM>(j), dy = slot_dy<NDIM>(j), dx = slot_dx<NDIM>(j);
         const int tlz = lz[i] + dz, tly = ly[i] + dy;
         const bool row_in = tlz >= 0 && tlz < G::TZ && tly >= 0 && tly < G::TY;
         uint32_t cand = row_in ? (lv & (dx > 0 ? 0x80000000u : (dx < 0 ? 1u : 0u))) : lv;
-        if (!cand) continue;
         const Idx gz = z0 + tlz, gy = y0 + tly;
-        if (gz < 0 || gz >= d0 || gy < 0 || gy >= d1) continue;
-        const int jo = slot_opp<NDIM>(j);
-        const uint32_t* rowf = a.flags + ((size_t)(gz * d1 + gy) * nseg) * SW + jo;
+        if (gz < 0 || gz >= d0 || gy < 0 || gy >= d1) cand = 0;
         uint32_t feed = 0;
-        const uint32_t inseg = cand & (dx > 0 ? 0x7fffffffu : (dx < 0 ? 0xfffffffeu : 0xffffffffu));
-        if (inseg) feed |= inseg & xshift(__ldg(rowf + (size_t)tx * SW), dx);
-        if (dx > 0 && (cand >> 31) && x0 + 32 < d2 && (__ldg(rowf + (size_t)(tx + 1) * SW) & 1u)) feed |= 0x80000000u;
-        if (dx < 0 && (cand & 1u) && tx > 0 && (__ldg(rowf + (size_t)(tx - 1) * SW) >> 31)) feed |= 1u;
-        while (feed) {
-          const int x = __ffs(feed) - 1;
+        if (cand) {
+          const int jo = slot_opp<NDIM>(j);
+          const uint32_t* rowf = a.flags + ((size_t)(gz * d1 + gy) * nseg) * SW + jo;
+          const uint32_t inseg = cand & (dx > 0 ? 0x7fffffffu : (dx < 0 ? 0xfffffffeu : 0xffffffffu));
+          if (inseg) feed |= inseg & xshift(__ldg(rowf + (size_t)tx * SW), dx);
+          if (dx > 0 && (cand >> 31) && x0 + 32 < d2 && (__ldg(rowf + (size_t)(tx + 1) * SW) & 1u)) feed |= 0x80000000u;
+          if (dx < 0 && (cand & 1u) && tx > 0 && (__ldg(rowf + (size_t)(tx - 1) * SW) >> 31)) feed |= 1u;
+        }
+        while (__any_sync(0xffffffffu, feed != 0)) {
+          const int x = feed ? __ffs(feed) - 1 : 0;
+          enqueue_warp<Idx>(a, (gz * d1 + gy) * d2 + x0 + x + dx, feed != 0, 2);
           feed &= feed - 1;
-          enqueue<Idx>(a, (gz * d1 + gy) * d2 + x0 + x + dx, 2);
         }
       }
     }
+    if (lane == 0) tile = atomicAdd(&a.ctr->tile_ticket, 1u);
+    tile = __shfl_sync(0xffffffffu, tile, 0);
   }
   if (tid == 0 && blockIdx.x == 0 && !a.skip_dense) a.ctr->pass_items[1] = (uint32_t)a.ntiles;
   grid.sync();
+  const uint64_t t_dense = (a.prof && tid == 0 && blockIdx.x == 0) ? gtimer() : 0;
 
   // ---- passes >= 2: sparse, point-level ------------------------------------
-  const int gtid = blockIdx.x * kSweepThreads + tid, gthreads = gridDim.x * kSweepThreads;
+  // Whole grid while the list is long; once it is short, block 0 finishes
+  // alone with block barriers (no grid-wide barrier per pass).
   int q = 2;
+  bool small = false;
   for (; q <= a.max_passes; ++q) {
     const unsigned long long n = *(volatile unsigned long long*)&a.ctr->list_count[q % 3];
     if (n == 0) break;
+    if (!small && n <= kSmallList) {
+      small = true;
+      if (blockIdx.x != 0) break;
+    }
     const UIdx* Lq = static_cast<const UIdx*>(a.plist) + (size_t)(q & 1) * a.cap;
-    for (unsigned long long i = gtid; i < n; i += gthreads) {
-      const Idx p = (Idx)__ldcg(&Lq[i]);
-      const uint32_t bit = 1u << ((uint32_t)p & 31u);
-      atomicAnd(&a.bitmap[(size_t)(q & 1) * a.bmw + ((UIdx)p >> 5)], ~bit);
-      const Idx z = p / plane, r2 = p - z * plane, y = r2 / d2, x = r2 - y * d2;
-      uint32_t fl = point_flags<NDIM>(a.flags + ((size_t)(z * d1 + y) * nseg + (size_t)(x >> 5)) * SW,
-                                      (uint32_t)x & 31u);
+    const unsigned long long wbase = small ? (unsigned long long)warp * 32 : (unsigned long long)gwarp * 32;
+    const unsigned long long wstep = small ? (unsigned long long)kSweepThreads : (unsigned long long)nwarps * 32;
+    for (unsigned long long ib = wbase; ib < n; ib += wstep) {
+      const unsigned long long i = ib + lane;
+      const bool act = i < n;
+      Idx p = 0, z = 0, y = 0, x = 0;
       uint32_t best = 0;
-      while (fl) {
-        const int j = __ffs(fl) - 1;
-        fl &= fl - 1;
-        const int e = (j < D ? j : j - D) + 1;
-        const Idx off = (NDIM == 3 ? (Idx)(e >> 2) * plane : (Idx)0) + (Idx)((e >> 1) & 1) * d2 + (Idx)(e & 1);
-        const uint32_t v = j < D ? __ldcg(&a.s[p + off]) + 1u : __ldcg(&a.s[p - off]);
-        best = v > best ? v : best;
+      bool raised = false;
+      if (act) {
+        p = (Idx)__ldcg(&Lq[i]);
+        const uint32_t bit = 1u << ((uint32_t)p & 31u);
+        atomicAnd(&a.bitmap[(size_t)(q & 1) * a.bmw + ((UIdx)p >> 5)], ~bit);
+        z = p / plane;
+        const Idx r2 = p - z * plane;
+        y = r2 / d2;
+        x = r2 - y * d2;
+        uint32_t fl = point_flags<NDIM>(a.flags + ((size_t)(z * d1 + y) * nseg + (size_t)(x >> 5)) * SW,
+                                        (uint32_t)x & 31u);
+        while (fl) {
+          const int j = __ffs(fl) - 1;
+          fl &= fl - 1;
+          const int e = (j < D ? j : j - D) + 1;
+          const Idx off = (NDIM == 3 ? (Idx)(e >> 2) * plane : (Idx)0) + (Idx)((e >> 1) & 1) * d2 + (Idx)(e & 1);
+          const uint32_t v = j < D ? __ldcg(&a.s[p + off]) + 1u : __ldcg(&a.s[p - off]);
+          best = v > best ? v : best;
+        }
+        if (best > __ldcg(&a.s[p])) {
+          const uint32_t old = atomicMax(&a.s[p], best);
+          raised = old < best;
+        }
       }
-      if (best <= __ldcg(&a.s[p])) continue;
-      const uint32_t old = atomicMax(&a.s[p], best);
-      if (old >= best) continue;
-      ++my_raised;
-      my_max = best > my_max ? best : my_max;
+      if (raised) {
+        ++my_raised;
+        my_max = best > my_max ? best : my_max;
+      }
+      if (!__any_sync(0xffffffffu, raised)) continue;
 #pragma unroll
       for (int j = 0; j < 2 * D; ++j) {
         const Idx qx = x + slot_dx<NDIM>(j), qy = y + slot_dy<NDIM>(j), qz = z + slot_dz<NDIM>(j);
-        if (qx < 0 || qx >= d2 || qy < 0 || qy >= d1 || qz < 0 || qz >= d0) continue;
-        const uint32_t w = __ldg(a.flags + ((size_t)(qz * d1 + qy) * nseg + (size_t)(qx >> 5)) * SW + slot_opp<NDIM>(j));
-        if ((w >> ((uint32_t)qx & 31u)) & 1u) enqueue<Idx>(a, p + slot_goff<NDIM, Idx>(j, plane, d2), q + 1);
+        bool v = raised && qx >= 0 && qx < d2 && qy >= 0 && qy < d1 && qz >= 0 && qz < d0;
+        if (v) {
+          const uint32_t w =
+              __ldg(a.flags + ((size_t)(qz * d1 + qy) * nseg + (size_t)(qx >> 5)) * SW + slot_opp<NDIM>(j));
+          v = (w >> ((uint32_t)qx & 31u)) & 1u;
+        }
+        enqueue_warp<Idx>(a, p + slot_goff<NDIM, Idx>(j, plane, d2), v, q + 1);
       }
     }
     if (tid == 0 && blockIdx.x == 0) {
@@ -606,9 +665,20 @@ __global__ void __launch_bounds__(kSweepThreads, 3) k_sweep(RepairArgs a) {
       if (q < kPassHist) a.ctr->pass_items[q] = (uint32_t)n;
       a.ctr->worklist_points += n;
     }
-    grid.sync();
+    if (small) {
+      __threadfence();  // the next pass reads the lists and s through L2
+      __syncthreads();
+    } else {
+      grid.sync();
+    }
   }
-  if (tid == 0 && blockIdx.x == 0) a.ctr->passes = (unsigned long long)(q - 1);
+  if (tid == 0 && blockIdx.x == 0) {
+    a.ctr->passes = (unsigned long long)(q - 1);
+    if (a.prof) {
+      a.ctr->phase[14] += t_dense - t_start;
+      a.ctr->phase[15] += gtimer() - t_dense;
+    }
+  }
   my_raised = __reduce_add_sync(0xffffffffu, my_raised);
   my_max = __reduce_max_sync(0xffffffffu, my_max);
   const unsigned lv32 = __reduce_add_sync(0xffffffffu, (unsigned)my_levels);
