@@ -134,6 +134,68 @@ const char* lopc_last_error_string(void);
 
 int lopc_abi_version(void);
 
+/* ---- Multi-GPU slab mode -----------------------------------
+ * The grid is split into R contiguous element ranges [b_r, b_{r+1}) of the
+ * linear order, rank r owning range r (one rank per GPU, one process each).
+ * Every inner boundary b_r must be a multiple of W = 16384/k (each chunk has
+ * one owner) and every range except the first and last must hold at least
+ * H = d1*d2 + d2 + 1 (3D) / d2 + 1 (2D) elements (halos come from adjacent
+ * ranks only); lopc_slab_partition gives a valid chunk-balanced split.
+ * lopc_compress_slab runs the repair on the rank's range plus its halo, then
+ * exchanges the halo subbins with rank r-1 / r+1 after every round until no
+ * subbin changes on any rank (one NCCL send/recv pair per neighbour and one
+ * u64 allreduce per round; the least fixpoint is unique, so the result is
+ * the single-GPU one), then encodes the rank's chunks.  Output per rank
+ * (out_local): its size-table slice (8 bytes per owned chunk) followed by its
+ * payload slice.  The single-GPU stream is
+ *   header(total) ‖ table slices in rank order ‖ payload slices in rank order,
+ * and *payload_offset is where this rank's payload slice starts in it.
+ * Device pointers only (in_slab, out_local, workspace).  Errors are agreed
+ * across ranks (every rank returns the worst code).  A NULL comm means
+ * world = 1.
+ */
+typedef struct lopc_comm lopc_comm;
+
+/* NCCL unique id (128 bytes) for lopc_comm_create; make it on one rank and
+ * broadcast it (e.g. torch.distributed.broadcast_object_list). */
+int lopc_comm_unique_id(void* id128);
+/* NCCL communicator on the current CUDA device (libnccl.so.2 via dlopen: the
+ * copy the process already loaded, e.g. torch's).  Collective over ranks. */
+int lopc_comm_create(lopc_comm** comm, int world, int rank, const void* id128);
+int lopc_comm_destroy(lopc_comm* comm);
+
+/* Default partition: world+1 chunk-aligned bounds, chunk-balanced.  Host only. */
+int lopc_slab_partition(int ndims, const uint64_t* dims, int dtype, int world, uint64_t* bounds);
+/* Host-side geometry of one range (for tests/bindings): info8 = {box start
+ * B0, box points, H, ghosts below, ghosts above, points sent down, points
+ * sent up, owned chunks}.  has_lo / has_hi: a neighbour exists below/above. */
+int lopc_slab_info(int ndims, const uint64_t* dims, int dtype, uint64_t e_begin, uint64_t e_end, int has_lo,
+                   int has_hi, uint64_t* info8);
+size_t lopc_slab_workspace_bytes(int ndims, const uint64_t* dims, int dtype, uint64_t e_begin, uint64_t e_end);
+/* Worst-case out_local bytes of a range. */
+size_t lopc_slab_bound(int ndims, const uint64_t* dims, int dtype, uint64_t e_begin, uint64_t e_end);
+/* The 64-byte stream header for a stream of total_bytes (host buffer). */
+int lopc_write_header(void* hdr64, int ndims, const uint64_t* dims, int dtype, double eps, uint64_t total_bytes);
+
+int lopc_compress_slab(lopc_comm* comm, const void* in_slab, int ndims, const uint64_t* dims, int dtype, double eps,
+                       uint64_t e_begin, uint64_t e_end, void* out_local, size_t* out_local_bytes,
+                       uint64_t* payload_offset, uint64_t* total_bytes, void* workspace, size_t workspace_bytes,
+                       void* stream);
+
+/* Decode the chunks of [e_begin, e_end) from a rank's out_local (table slice
+ * ‖ payload slice, local_bytes long), given the stream header (host).  No
+ * communication.  out_slab receives e_end - e_begin values. */
+size_t lopc_decompress_slab_workspace_bytes(uint64_t n_chunks_local);
+int lopc_decompress_slab(const void* hdr64_host, const void* local, size_t local_bytes, uint64_t e_begin,
+                         uint64_t e_end, void* out_slab, size_t out_capacity, void* workspace, size_t workspace_bytes,
+                         void* stream);
+
+/* Test hook (single device): the slab algorithm for nslabs ranges (bounds:
+ * nslabs+1 entries) in one call, halos exchanged by device copies, writing
+ * the whole stream to out (device).  Allocates its own scratch. */
+int lopc_compress_slabs_local(const void* in, int ndims, const uint64_t* dims, int dtype, double eps, int nslabs,
+                              const uint64_t* bounds, void* out, size_t* out_bytes);
+
 #ifdef __cplusplus
 }
 #endif

@@ -246,12 +246,7 @@ void write_header_host(uint8_t* h, const Shape& s, double eps, uint64_t total) {
   memcpy(h + 56, &total, 8);
 }
 
-// Steps a1-a3 (quantize, flags, repair to the fixpoint) on device input.
-int run_repair(const Shape& sh, const void* x, double eps, uint8_t* ws, const CLayout& L, cudaStream_t st, Timer& tm,
-               Counters* hc) {
-  DevInfo* di;
-  int rc = dev_info(di);
-  if (rc) return rc;
+RepairArgs make_repair_args(const Shape& sh, const void* x, double eps, uint8_t* ws, const CLayout& L) {
   RepairArgs ra{};
   ra.x = x;
   ra.flags = reinterpret_cast<uint32_t*>(ws + L.flags);
@@ -277,17 +272,16 @@ int run_repair(const Shape& sh, const void* x, double eps, uint8_t* ws, const CL
   ra.own_hi = (int64_t)sh.n;
   ra.skip_dense = 0;
   ra.prof = g_timing >= 2;
+  return ra;
+}
+
+bool use_i32(const Shape& sh) { return sh.n < (1ull << 31) - (1ull << 24); }
+
+// a1 + a2: k_quant_flags over the tile grid.
+int launch_quant_flags(const Shape& sh, const RepairArgs& ra, const CLayout& L, cudaStream_t st) {
   const dim3 tgrid((unsigned)L.ntx, (unsigned)L.nty, (unsigned)L.ntz);
-  const bool i32 = sh.n < (1ull << 31) - (1ull << 24);
-  int occ = sh.ndims == 3 ? (i32 ? di->occ_sweep3 : di->occ_sweep3w) : (i32 ? di->occ_sweep2 : di->occ_sweep2w);
-  uint64_t grid = (uint64_t)occ * di->sms;
-  if (grid > L.ntiles) grid = L.ntiles;
-  if (grid < 1) grid = 1;
-  void* kargs[] = {&ra};
 #define QR(TT, ND, IX) k_quant_flags<TT, ND, IX><<<tgrid, kRepairThreads, quant_flags_smem<TT, ND>(), st>>>(ra)
-#define SW(ND, IX)                                                                                               \
-  CK(cudaLaunchCooperativeKernel((void*)k_sweep<ND, IX>, dim3((unsigned)grid), dim3(kSweepThreads), kargs, 0, st))
-  if (i32) {
+  if (use_i32(sh)) {
     if (sh.dtype == LOPC_F32) {
       if (sh.ndims == 3) QR(float, 3, int32_t); else QR(float, 2, int32_t);
     } else {
@@ -300,15 +294,41 @@ int run_repair(const Shape& sh, const void* x, double eps, uint8_t* ws, const CL
       if (sh.ndims == 3) QR(double, 3, int64_t); else QR(double, 2, int64_t);
     }
   }
+#undef QR
   CK(cudaGetLastError());
-  tm.mark();
+  return LOPC_OK;
+}
+
+// a3: one cooperative k_sweep launch (dense pass unless ra.skip_dense).
+int launch_sweep(const Shape& sh, RepairArgs& ra, const CLayout& L, cudaStream_t st) {
+  DevInfo* di;
+  int rc = dev_info(di);
+  if (rc) return rc;
+  const bool i32 = use_i32(sh);
+  int occ = sh.ndims == 3 ? (i32 ? di->occ_sweep3 : di->occ_sweep3w) : (i32 ? di->occ_sweep2 : di->occ_sweep2w);
+  uint64_t grid = (uint64_t)occ * di->sms;
+  if (grid > L.ntiles) grid = L.ntiles;
+  if (grid < 1) grid = 1;
+  void* kargs[] = {&ra};
+#define SW(ND, IX) \
+  CK(cudaLaunchCooperativeKernel((void*)k_sweep<ND, IX>, dim3((unsigned)grid), dim3(kSweepThreads), kargs, 0, st))
   if (i32) {
     if (sh.ndims == 3) SW(3, int32_t); else SW(2, int32_t);
   } else {
     if (sh.ndims == 3) SW(3, int64_t); else SW(2, int64_t);
   }
-#undef QR
 #undef SW
+  return LOPC_OK;
+}
+
+// Steps a1-a3 (quantize, flags, repair to the fixpoint) on device input.
+int run_repair(const Shape& sh, const void* x, double eps, uint8_t* ws, const CLayout& L, cudaStream_t st, Timer& tm,
+               Counters* hc) {
+  RepairArgs ra = make_repair_args(sh, x, eps, ws, L);
+  int rc = launch_quant_flags(sh, ra, L, st);
+  if (rc) return rc;
+  tm.mark();
+  if ((rc = launch_sweep(sh, ra, L, st))) return rc;
   tm.mark();
   (void)hc;
   return LOPC_OK;
@@ -498,6 +518,7 @@ int lopc_compress_ex(const void* in, int ndims, const uint64_t* dims, int dtype,
   sa.off = reinterpret_cast<uint64_t*>(ws + L.off);
   sa.state = reinterpret_cast<uint64_t*>(ws + L.state);
   sa.ctr = dctr;
+  sa.base = kHdrBytes + 8 * sh.C;
   k_chunk_scan<<<(unsigned)((sh.C + kScanTile - 1) / kScanTile), kScanThreads, 0, st>>>(sa);
   CK(cudaGetLastError());
   PlaceArgs pa{};
@@ -505,6 +526,8 @@ int lopc_compress_ex(const void* in, int ndims, const uint64_t* dims, int dtype,
   pa.sizes = ea.sizes;
   pa.off = sa.off;
   pa.out = dst;
+  pa.table = dst + kHdrBytes;
+  pa.header = 1;
   pa.out_cap = host_out ? (kHdrBytes + 8 * sh.C + 2ull * kChunkBytes * sh.C) : cap;
   pa.ctr = dctr;
   pa.C = (uint32_t)sh.C;
@@ -667,6 +690,9 @@ int lopc_decompress_ex(const void* in, size_t in_bytes, void* out, size_t out_ca
   da.out = host_out ? (void*)(ws + o_out) : out;
   da.out_cap = out_capacity;
   da.off = sa.off;
+  da.table = reinterpret_cast<const uint32_t*>(src + kHdrBytes);
+  da.base = src;
+  da.c_begin = 0;
   da.state_cap = cmax;
   da.prof = g_timing >= 2;
   da.ctr = reinterpret_cast<Counters*>(ws + o_ctr);
@@ -716,3 +742,5 @@ int lopc_decompress(const void* in, size_t in_bytes, void* out, size_t out_capac
 }
 
 }  // extern "C"
+
+#include "lopc_slab.cuh"

@@ -823,6 +823,7 @@ struct ScanArgs {
   Counters* ctr;
   int validate;           // decode: check 4 <= size <= 16384, size % 4 == 0
   uint64_t expect_total;  // decode: the stream length
+  uint64_t base;          // sizes mode: offset of the first payload (64 + 8C, or 0 / 8C in slab mode)
 };
 
 __global__ void __launch_bounds__(kScanThreads) k_chunk_scan(ScanArgs a) {
@@ -847,7 +848,7 @@ __global__ void __launch_bounds__(kScanThreads) k_chunk_scan(ScanArgs a) {
   const uint32_t tile = tile_s, C = C_s;
   if ((uint64_t)tile * kScanTile >= C) return;  // beyond the last tile: nobody waits on it
   const uint32_t* sizes = a.in ? reinterpret_cast<const uint32_t*>(a.in + kHdrBytes) : a.sizes;
-  const uint64_t base = (uint64_t)kHdrBytes + 8ull * C;
+  const uint64_t base = a.in ? (uint64_t)kHdrBytes + 8ull * C : a.base;
   const uint32_t c0 = tile * kScanTile + tid * kScanPer;
   unsigned long long v[kScanPer];
   unsigned long long run = 0;
@@ -894,7 +895,9 @@ struct PlaceArgs {
   const uint8_t* stage;
   const uint32_t* sizes;
   const uint64_t* off;
-  uint8_t* out;
+  uint8_t* out;          // payload c goes to out + off[c]
+  uint8_t* table;        // size-table entry c goes to table + 8c
+  int header;            // write the 64-byte header at out (whole-stream mode)
   uint64_t out_cap;
   Counters* ctr;
   uint32_t C;
@@ -918,11 +921,11 @@ __global__ void __launch_bounds__(256) k_place(PlaceArgs a) {
     for (uint32_t i = lane; i < bs / 4; i += 32) dst[i] = __ldcs(&src[i]);
     for (uint32_t i = lane; i < ss / 4; i += 32) dst[bs / 4 + i] = __ldcs(&src[kChunkBytes / 4 + i]);
     if (lane == 0) {
-      uint32_t* tab = reinterpret_cast<uint32_t*>(a.out + kHdrBytes + 8ull * c);
+      uint32_t* tab = reinterpret_cast<uint32_t*>(a.table + 8ull * c);
       tab[0] = bs;
       tab[1] = ss;
     }
-    if (c == 0 && lane == 0) {
+    if (a.header && c == 0 && lane == 0) {
       uint32_t* h32 = reinterpret_cast<uint32_t*>(a.out);
       uint64_t* h64 = reinterpret_cast<uint64_t*>(a.out);
       h32[0] = 0x43504f4cu;  // "LOPC"
@@ -942,17 +945,6 @@ __global__ void __launch_bounds__(256) k_place(PlaceArgs a) {
 // ---------------------------------------------------------------------------
 // k_decode (persistent; dtype from the stream header)
 // ---------------------------------------------------------------------------
-struct DecodeArgs {
-  const uint8_t* in;
-  uint64_t in_bytes;
-  void* out;
-  uint64_t out_cap;
-  const uint64_t* off;  // chunk payload offsets from k_chunk_scan
-  uint64_t state_cap;   // chunk entries available in the workspace
-  Counters* ctr;
-  int prof;             // diagnostic phase clocks
-};
-
 struct Hdr {
   int dtype, ndims;
   uint64_t d0, d1, d2, n;
@@ -962,7 +954,24 @@ struct Hdr {
   uint32_t err;
 };
 
+struct DecodeArgs {
+  const uint8_t* in;    // whole-stream mode: the stream (header validated on the device)
+  uint64_t in_bytes;
+  void* out;            // chunk c (global index) decodes to out + c W
+  uint64_t out_cap;
+  const uint64_t* off;  // payload offsets of the chunks [c_begin, c_begin + c_count), from k_chunk_scan
+  const uint32_t* table;  // their (bin, sub) size pairs
+  const uint8_t* base;  // payload of local chunk l at base + off[l]
+  uint64_t c_begin, c_count;
+  uint64_t state_cap;   // chunk entries available in the workspace
+  Counters* ctr;
+  int prof;             // diagnostic phase clocks
+  int slab;             // slab mode: header given (host-validated), no whole-stream checks
+  Hdr given;
+};
+
 __device__ __forceinline__ Hdr parse_header(const DecodeArgs& a) {
+  if (a.slab) return a.given;
   Hdr h{};
   h.ok = false;
   h.err = kErrCorrupt;
@@ -1156,7 +1165,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kCodecThreads, 4) k_
     return;
   }
   if (h32_err(a)) return;  // k_chunk_scan flagged the table
-  const uint32_t* tab = reinterpret_cast<const uint32_t*>(a.in + kHdrBytes);
+  const uint64_t ncnk = a.slab ? a.c_count : (uint64_t)h.C;
   const DecSmem* s0 = cl.map_shared_rank(&sm, 0);
   DecSmem* s1 = cl.map_shared_rank(&sm, 1);
   if (tid == 0) sm.bad = 0;  // sticky: a corrupt chunk fails the whole call
@@ -1169,20 +1178,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kCodecThreads, 4) k_
       }
     }
     cl.sync();  // ticket visible; the partner finished reading our words
-    const uint32_t c = sm.ticket;  // local copy: the partner may exit after this barrier
-    if (c >= h.C) break;
-    const uint32_t sz = tab[2 * c + r];
-    const uint8_t* p = a.in + a.off[c] + (r ? tab[2 * c] : 0u);
+    const uint32_t l = sm.ticket;  // local copy: the partner may exit after this barrier
+    if (l >= ncnk) break;
+    const uint32_t sz = a.table[2 * l + r];
+    const uint8_t* p = a.base + a.off[l] + (r ? a.table[2 * l] : 0u);
     if (h.dtype == 0)
       decode_stream<float>(a, p, sz, r != 0, sm);
     else
       decode_stream<double>(a, p, sz, r != 0, sm);
     cl.sync();
+    const uint64_t c = a.c_begin + l;
     if (!s0->bad && !s1->bad) {
       if (h.dtype == 0)
-        reconstruct_half<float>(a, h, c, r, s0->Wd, s1->Wd);
+        reconstruct_half<float>(a, h, (uint32_t)c, r, s0->Wd, s1->Wd);
       else
-        reconstruct_half<double>(a, h, c, r, s0->Wd, s1->Wd);
+        reconstruct_half<double>(a, h, (uint32_t)c, r, s0->Wd, s1->Wd);
     }
   }
 }

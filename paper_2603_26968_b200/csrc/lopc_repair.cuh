@@ -115,6 +115,7 @@ struct Counters {
   unsigned long long list_count[3];  // point worklists (rotating)
   uint32_t pass_items[kPassHist];    // [1] tiles of the dense pass, [q>1] worklist points of pass q
   unsigned long long phase[16];      // diagnostic: SM cycles per codec phase (lopc_set_timing(2))
+  unsigned long long ghost_changed;  // slab mode: ghosts raised by the last k_ghost_inject
 };
 
 // Diagnostic phase clock: thread 0 of a block adds the cycles since the last
@@ -685,6 +686,56 @@ __global__ void __launch_bounds__(kSweepThreads, 3) k_sweep(RepairArgs a) {
   if (lane == 0 && lv32) atomicAdd(&a.ctr->inner_iters, (unsigned long long)lv32 / 32ull);
   if (lane == 0 && my_raised) atomicAdd(&a.ctr->raised, (unsigned long long)my_raised);
   if (lane == 0 && my_max) atomicMax(&a.ctr->max_s, my_max);
+}
+
+// Slab mode: ghost points (box points owned by a neighbour
+// rank) have no incoming arcs here; their subbins arrive from the owner after
+// each repair round.  A ghost whose value rose is written and its successors
+// (points with an arc from it) are enqueued for the next sparse pass (pass 2
+// of the next k_sweep launch, skip_dense).  ctr->raised counts the ghosts that
+// changed (the round's termination term, summed over ranks).
+template <int NDIM, typename Idx>
+__global__ void __launch_bounds__(256) k_ghost_inject(RepairArgs a, const uint32_t* __restrict__ recv, int64_t g0,
+                                                      int64_t count) {
+  using G = Geo<NDIM>;
+  constexpr int D = G::D;
+  constexpr int SW = G::SW;
+  const int lane = threadIdx.x & 31;
+  const Idx d0 = (Idx)a.d0, d1 = (Idx)a.d1, d2 = (Idx)a.d2, plane = d1 * d2;
+  const size_t nseg = (size_t)a.nseg;
+  unsigned changed = 0;
+  const int64_t wstep = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t ib = (int64_t)(blockIdx.x * blockDim.x + (threadIdx.x & ~31)); ib < count; ib += wstep) {
+    const int64_t i = ib + lane;
+    bool up = false;
+    Idx p = 0, z = 0, y = 0, x = 0;
+    if (i < count) {
+      p = (Idx)(g0 + i);
+      const uint32_t v = __ldg(&recv[i]);
+      if (v > a.s[p]) {
+        a.s[p] = v;
+        up = true;
+        ++changed;
+      }
+      z = p / plane;
+      const Idx r2 = p - z * plane;
+      y = r2 / d2;
+      x = r2 - y * d2;
+    }
+    if (!__any_sync(0xffffffffu, up)) continue;
+#pragma unroll
+    for (int j = 0; j < 2 * D; ++j) {
+      const Idx qx = x + slot_dx<NDIM>(j), qy = y + slot_dy<NDIM>(j), qz = z + slot_dz<NDIM>(j);
+      bool v = up && qx >= 0 && qx < d2 && qy >= 0 && qy < d1 && qz >= 0 && qz < d0;
+      if (v) {
+        const uint32_t w = __ldg(a.flags + ((size_t)(qz * d1 + qy) * nseg + (size_t)(qx >> 5)) * SW + slot_opp<NDIM>(j));
+        v = (w >> ((uint32_t)qx & 31u)) & 1u;
+      }
+      enqueue_warp<Idx>(a, p + slot_goff<NDIM, Idx>(j, plane, d2), v, 2);
+    }
+  }
+  changed = __reduce_add_sync(0xffffffffu, changed);
+  if (lane == 0 && changed) atomicAdd(&a.ctr->ghost_changed, (unsigned long long)changed);
 }
 
 // Debug/parity: bit-plane flags -> one u16 per point.

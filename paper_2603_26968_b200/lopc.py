@@ -211,3 +211,132 @@ def last_stats() -> dict:
     d["pass_items"] = [int(v) for v in st.pass_items]
     d["phase_cycles"] = [int(v) for v in st.phase_cycles]
     return d
+
+
+# ---- multi-GPU slab mode (include/lopc.h) --------------------
+def _slab_syms(L):
+    if getattr(L, "_slab_ready", False):
+        return L
+    P, I, D, SZ, U64, U64P = C.c_void_p, C.c_int, C.c_double, C.c_size_t, C.c_uint64, C.POINTER(C.c_uint64)
+    L.lopc_comm_unique_id.argtypes = [P]
+    L.lopc_comm_create.argtypes = [C.POINTER(P), I, I, P]
+    L.lopc_comm_destroy.argtypes = [P]
+    L.lopc_slab_partition.argtypes = [I, U64P, I, I, U64P]
+    L.lopc_slab_info.argtypes = [I, U64P, I, U64, U64, I, I, U64P]
+    L.lopc_slab_workspace_bytes.argtypes = [I, U64P, I, U64, U64]
+    L.lopc_slab_workspace_bytes.restype = SZ
+    L.lopc_slab_bound.argtypes = [I, U64P, I, U64, U64]
+    L.lopc_slab_bound.restype = SZ
+    L.lopc_write_header.argtypes = [P, I, U64P, I, D, U64]
+    L.lopc_compress_slab.argtypes = [P, P, I, U64P, I, D, U64, U64, P, C.POINTER(SZ), U64P, U64P, P, SZ, P]
+    L.lopc_decompress_slab_workspace_bytes.argtypes = [U64]
+    L.lopc_decompress_slab_workspace_bytes.restype = SZ
+    L.lopc_decompress_slab.argtypes = [P, P, SZ, U64, U64, P, SZ, P, SZ, P]
+    L.lopc_compress_slabs_local.argtypes = [P, I, U64P, I, D, I, U64P, P, C.POINTER(SZ)]
+    for f in ("lopc_comm_unique_id", "lopc_comm_create", "lopc_comm_destroy", "lopc_slab_partition", "lopc_slab_info",
+              "lopc_write_header", "lopc_compress_slab", "lopc_decompress_slab", "lopc_compress_slabs_local"):
+        getattr(L, f).restype = I
+    L._slab_ready = True
+    return L
+
+
+def slab_partition(shape, dtype, world: int) -> list[int]:
+    """Chunk-aligned, chunk-balanced range bounds (world+1 entries)."""
+    L = _slab_syms(load(False))
+    b = (C.c_uint64 * (world + 1))()
+    _check(L.lopc_slab_partition(len(shape), _dims(shape), _dtype_code(dtype), world, b), "lopc_slab_partition")
+    return [int(v) for v in b]
+
+
+def slab_info(shape, dtype, e_begin: int, e_end: int, has_lo: bool, has_hi: bool) -> dict:
+    L = _slab_syms(load(False))
+    v = (C.c_uint64 * 8)()
+    _check(L.lopc_slab_info(len(shape), _dims(shape), _dtype_code(dtype), e_begin, e_end, int(has_lo), int(has_hi), v),
+           "lopc_slab_info")
+    keys = ("box_begin", "box_points", "halo", "ghosts_lo", "ghosts_hi", "send_lo", "send_hi", "chunks")
+    return dict(zip(keys, (int(t) for t in v)))
+
+
+def write_header(shape, dtype, eps: float, total_bytes: int) -> bytes:
+    L = _slab_syms(load(False))
+    h = C.create_string_buffer(64)
+    _check(L.lopc_write_header(h, len(shape), _dims(shape), _dtype_code(dtype), float(eps), total_bytes),
+           "lopc_write_header")
+    return h.raw
+
+
+def comm_unique_id() -> bytes:
+    L = _slab_syms(load())
+    b = C.create_string_buffer(128)
+    _check(L.lopc_comm_unique_id(b), "lopc_comm_unique_id")
+    return b.raw
+
+
+class Comm:
+    """NCCL communicator of the slab mode (one rank per GPU/process)."""
+
+    def __init__(self, world: int, rank: int, uid: bytes):
+        L = _slab_syms(load())
+        self.world, self.rank = world, rank
+        self.h = C.c_void_p()
+        buf = C.create_string_buffer(uid, 128)
+        _check(L.lopc_comm_create(C.byref(self.h), world, rank, buf), "lopc_comm_create")
+
+    def close(self):
+        if self.h:
+            load(False).lopc_comm_destroy(self.h)
+            self.h = C.c_void_p()
+
+
+def compress_slab(comm, x_slab: torch.Tensor, shape, eps: float, e_begin: int, e_end: int, out=None):
+    """lopc_compress_slab: x_slab = the rank's values [e_begin, e_end) of the
+    global grid `shape` (device).  Returns (out_local view, payload_offset,
+    total_bytes)."""
+    L = _slab_syms(load())
+    x_slab = x_slab.contiguous()
+    dt = _dtype_code(x_slab.dtype)
+    cap = L.lopc_slab_bound(len(shape), _dims(shape), dt, e_begin, e_end)
+    if out is None:
+        out = torch.empty(cap, dtype=torch.uint8, device=x_slab.device)
+    need = L.lopc_slab_workspace_bytes(len(shape), _dims(shape), dt, e_begin, e_end)
+    ws = _workspace(need, x_slab.device)
+    nb = C.c_size_t(out.numel())
+    po, tot = C.c_uint64(), C.c_uint64()
+    with torch.cuda.device(x_slab.device):
+        rc = L.lopc_compress_slab(comm.h if comm is not None else None, C.c_void_p(x_slab.data_ptr()), len(shape),
+                                  _dims(shape), dt, float(eps), e_begin, e_end, C.c_void_p(out.data_ptr()),
+                                  C.byref(nb), C.byref(po), C.byref(tot), C.c_void_p(ws.data_ptr()), ws.numel(),
+                                  _stream(x_slab.device))
+    _check(rc, "lopc_compress_slab")
+    return out[: nb.value], int(po.value), int(tot.value)
+
+
+def decompress_slab(header: bytes, local: torch.Tensor, e_begin: int, e_end: int, dtype, out=None) -> torch.Tensor:
+    L = _slab_syms(load())
+    W = 16384 // (4 if dtype == torch.float32 else 8)
+    if out is None:
+        out = torch.empty(e_end - e_begin, dtype=dtype, device=local.device)
+    cl = (e_end - e_begin + W - 1) // W
+    ws = _workspace(L.lopc_decompress_slab_workspace_bytes(cl), local.device)
+    hb = C.create_string_buffer(header, 64)
+    with torch.cuda.device(local.device):
+        rc = L.lopc_decompress_slab(hb, C.c_void_p(local.data_ptr()), local.numel(), e_begin, e_end,
+                                    C.c_void_p(out.data_ptr()), out.numel() * out.element_size(),
+                                    C.c_void_p(ws.data_ptr()), ws.numel(), _stream(local.device))
+    _check(rc, "lopc_decompress_slab")
+    return out
+
+
+def compress_slabs_local(x: torch.Tensor, eps: float, bounds) -> torch.Tensor:
+    """Test hook: the slab algorithm over len(bounds)-1 ranges on one device."""
+    L = _slab_syms(load())
+    x = x.contiguous()
+    cap = compress_bound(x.shape, x.dtype)
+    out = torch.empty(cap, dtype=torch.uint8, device=x.device)
+    b = (C.c_uint64 * len(bounds))(*bounds)
+    nb = C.c_size_t(cap)
+    with torch.cuda.device(x.device):
+        rc = L.lopc_compress_slabs_local(C.c_void_p(x.data_ptr()), x.dim(), _dims(x.shape), _dtype_code(x.dtype),
+                                         float(eps), len(bounds) - 1, b, C.c_void_p(out.data_ptr()), C.byref(nb))
+    _check(rc, "lopc_compress_slabs_local")
+    return out[: nb.value]
