@@ -3,4 +3,4 @@ chunked lossless coding, and the matching decoder, as hand-written sm_100a
 CUDA kernels behind the C-ABI in include/lopc.h."""
 from .lopc import (Comm, LopcError, comm_unique_id, compress, compress_bound, compress_slab,  # noqa: F401
                    compress_slabs_local, decompress, decompress_slab, last_stats, load, repair, set_timing,
-                   slab_info, slab_partition, stream_info, write_header)
+                   slab_bound, slab_info, slab_partition, stream_info, write_header)

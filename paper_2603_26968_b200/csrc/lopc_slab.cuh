@@ -168,7 +168,7 @@ struct Slab {
     return launch_sweep(geo.box, ra, lay.L, st);
   }
   // encode the owned chunks; out_local = table slice (8 C_local) ‖ payloads
-  int encode(uint8_t* out_local, size_t cap) {
+  int encode(uint8_t* out_local, size_t cap, Timer* tm = nullptr) {
     const Shape& g = geo.g;
     EncodeArgs ea{};
     ea.x = x_own;
@@ -193,6 +193,7 @@ struct Slab {
     else
       k_encode<double><<<(unsigned)(2 * geo.C_local), kCodecThreads, smem, st>>>(ea);
     CK(cudaGetLastError());
+    if (tm) tm->mark();
     ScanArgs sa{};
     sa.sizes = ea.sizes;
     sa.C = (uint32_t)geo.C_local;
@@ -425,6 +426,9 @@ int lopc_compress_slab(lopc_comm* comm, const void* in_slab, int ndims, const ui
   sl.x_own = in_slab;
   sl.eps = eps;
   sl.st = st;
+  Timer tm;
+  if ((rc = tm.init(st))) return rc;
+  tm.mark();  // 0
   if ((rc = sl.setup())) return rc;
   const SlabGeo& G = sl.geo;
   const int lo = rank - 1, hi = rank + 1;
@@ -444,7 +448,10 @@ int lopc_compress_slab(lopc_comm* comm, const void* in_slab, int ndims, const ui
     if (G.glo) CK(cudaMemcpyAsync(sl.ghost_lo_ptr(sl.xbox(), g.k), sl.recv_lo(), G.glo * g.k, cudaMemcpyDeviceToDevice, st));
     if (G.ghi) CK(cudaMemcpyAsync(sl.ghost_hi_ptr(sl.xbox(), g.k), sl.recv_hi(), G.ghi * g.k, cudaMemcpyDeviceToDevice, st));
   }
-  if ((rc = sl.round1())) return rc;
+  tm.mark();  // 1
+  if ((rc = launch_quant_flags(G.box, sl.ra, sl.lay.L, st))) return rc;
+  tm.mark();  // 2
+  if ((rc = launch_sweep(G.box, sl.ra, sl.lay.L, st))) return rc;
   uint64_t rounds = 1;
   while (world > 1) {
     if ((rc = halo(reinterpret_cast<uint8_t*>(sl.s()), 4, ncclUint32))) return rc;
@@ -458,9 +465,19 @@ int lopc_compress_slab(lopc_comm* comm, const void* in_slab, int ndims, const ui
     if ((rc = sl.sweep_sparse())) return rc;
     ++rounds;
   }
-  if ((rc = sl.encode(static_cast<uint8_t*>(out_local), *out_local_bytes))) return rc;
+  tm.mark();  // 3
+  if ((rc = sl.encode(static_cast<uint8_t*>(out_local), *out_local_bytes, &tm))) return rc;  // mark 4
+  tm.mark();  // 5
   CK(cudaMemcpyAsync(hc, sl.dctr(), sizeof(Counters), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
+  if (tm.on) {
+    g_stats.timing_valid = 1;
+    g_stats.ms_quant_repair = tm.ms(1, 2);
+    g_stats.ms_sweep = tm.ms(2, 3);  // all repair rounds, halo exchanges included
+    g_stats.ms_encode = tm.ms(3, 4);
+    g_stats.ms_place = tm.ms(4, 5);
+    g_stats.ms_total = tm.ms(0, 5);
+  }
   uint64_t mine[2] = {hc->total_bytes, (uint64_t)err_rank(map_err(hc->err))};
   std::vector<uint64_t> all(2 * world);
   if (world > 1) {
@@ -664,8 +681,12 @@ int lopc_decompress_slab(const void* hdr64_host, const void* local, size_t local
   sa.validate = 1;
   sa.expect_total = local_bytes;
   sa.base = 8 * CL;
+  Timer tm;
+  if ((rc = tm.init(st))) return rc;
+  tm.mark();  // 0
   k_chunk_scan<<<(unsigned)((CL + kScanTile - 1) / kScanTile), kScanThreads, 0, st>>>(sa);
   CK(cudaGetLastError());
+  tm.mark();  // 1
   DecodeArgs da{};
   da.in = src;
   da.in_bytes = local_bytes;
@@ -693,8 +714,17 @@ int lopc_decompress_slab(const void* hdr64_host, const void* local, size_t local
   if (grid > 2 * CL) grid = (unsigned)(2 * CL);
   k_decode<<<grid, kCodecThreads, sizeof(DecSmem), st>>>(da);
   CK(cudaGetLastError());
+  tm.mark();  // 2
   CK(cudaMemcpyAsync(hc, ws, sizeof(Counters), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
+  g_stats = lopc_stats{};
+  g_stats.launches = 2;
+  if (tm.on) {
+    g_stats.timing_valid = 1;
+    g_stats.ms_place = tm.ms(0, 1);
+    g_stats.ms_decode = tm.ms(1, 2);
+    g_stats.ms_total = tm.ms(0, 2);
+  }
   return map_err(hc->err);
 }
 

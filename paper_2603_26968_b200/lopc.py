@@ -257,6 +257,11 @@ def slab_info(shape, dtype, e_begin: int, e_end: int, has_lo: bool, has_hi: bool
     return dict(zip(keys, (int(t) for t in v)))
 
 
+def slab_bound(shape, dtype, e_begin: int, e_end: int) -> int:
+    L = _slab_syms(load(False))
+    return int(L.lopc_slab_bound(len(shape), _dims(shape), _dtype_code(dtype), e_begin, e_end))
+
+
 def write_header(shape, dtype, eps: float, total_bytes: int) -> bytes:
     L = _slab_syms(load(False))
     h = C.create_string_buffer(64)
