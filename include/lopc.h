@@ -134,6 +134,37 @@ const char* lopc_last_error_string(void);
 
 int lopc_abi_version(void);
 
+/* ---- Checker (SURVEY §8(d.1) k_check; NEXT f3 error statistics) ------------
+ * x, y: device arrays of the same grid.  order_violations: star edges
+ * {p, p+e} (each once) with non-NaN x at both ends whose SoS order (ord, then
+ * index) differs in y (or y is NaN there).  bound_violations: escaped points
+ * not bit-identical, or regular points without 0 <= x - y <= eps exactly.
+ * max_abs_err / sum_sq_err over the regular points (PSNR = 20 log10(range) -
+ * 10 log10(sum_sq_err / n_regular)).  Uses the first 256 bytes of workspace. */
+typedef struct {
+  uint64_t order_violations;
+  uint64_t bound_violations;
+  uint64_t n_regular;
+  double max_abs_err;
+  double sum_sq_err;
+} lopc_check_result;
+int lopc_check(const void* x, const void* y, int ndims, const uint64_t* dims, int dtype, double eps,
+               lopc_check_result* res, void* workspace, size_t workspace_bytes, void* stream);
+
+/* ---- NOA error bound on the device (row a0) ---------------
+ * lopc_value_range: min and max over the finite values of x (device pointer,
+ * one read pass; NaN and +-Inf skipped), returned as doubles, and their count.
+ * Uses the first 256 bytes of `workspace`.  Blocks (one 24-byte D2H read).
+ * lopc_noa_eps: eps = rel * (max - min) in double, or rel if there is no
+ * finite value or max == min (P:112 NOA).  lopc_compress_noa = both, then
+ * lopc_compress_ex with that eps (reported in *eps_used); workspace as for
+ * lopc_compress_ex. */
+int lopc_value_range(const void* in, int ndims, const uint64_t* dims, int dtype, double* vmin, double* vmax,
+                     uint64_t* n_finite, void* workspace, size_t workspace_bytes, void* stream);
+double lopc_noa_eps(double vmin, double vmax, uint64_t n_finite, double rel);
+int lopc_compress_noa(const void* in, int ndims, const uint64_t* dims, int dtype, double rel, void* out,
+                      size_t* out_bytes, double* eps_used, void* workspace, size_t workspace_bytes, void* stream);
+
 /* ---- Multi-GPU slab mode -----------------------------------
  * The grid is split into R contiguous element ranges [b_r, b_{r+1}) of the
  * linear order, rank r owning range r (one rank per GPU, one process each).

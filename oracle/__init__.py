@@ -77,6 +77,10 @@ def lib():
         L.lopc_ref_encode_chunk.restype = I
         L.lopc_ref_certify.argtypes = [P, I, U64P, I, D, P]
         L.lopc_ref_certify.restype = C.c_uint64
+        L.lopc_ref_value_range.argtypes = [P, C.c_uint64, I, C.POINTER(D), C.POINTER(D)]
+        L.lopc_ref_value_range.restype = C.c_uint64
+        L.lopc_ref_noa_eps.argtypes = [P, C.c_uint64, I, D]
+        L.lopc_ref_noa_eps.restype = D
         _lib = L
     return _lib
 
@@ -276,3 +280,17 @@ def certify(x: np.ndarray, eps: float, s: np.ndarray) -> int:
     x = np.ascontiguousarray(x)
     s = np.ascontiguousarray(s, dtype=np.uint32)
     return int(lib().lopc_ref_certify(_ptr(x), x.ndim, _dims(x), _dt(x), eps, _ptr(s)))
+
+
+def value_range(x: np.ndarray):
+    """Row a0: (min, max, count) over the finite values, as doubles."""
+    x = np.ascontiguousarray(x)
+    lo, hi = C.c_double(), C.c_double()
+    n = lib().lopc_ref_value_range(_ptr(x), x.size, _dt(x), C.byref(lo), C.byref(hi))
+    return lo.value, hi.value, int(n)
+
+
+def noa_eps(x: np.ndarray, rel: float) -> float:
+    """Row a0: eps = rel * (max - min) over the finite values."""
+    x = np.ascontiguousarray(x)
+    return float(lib().lopc_ref_noa_eps(_ptr(x), x.size, _dt(x), float(rel)))

@@ -1061,3 +1061,26 @@ uint64_t lopc_ref_certify(const void* x, int ndims, const uint64_t* dims, int dt
   field_free(&f);
   return bad;
 }
+
+/* ---- row a0: NOA range -------------------------------------------- */
+uint64_t lopc_ref_value_range(const void* x, uint64_t n, int dtype, double* vmin, double* vmax) {
+  uint64_t cnt = 0;
+  double lo = 0.0, hi = 0.0;
+  for (uint64_t i = 0; i < n; i++) {
+    double v = value_at(x, i, dtype);
+    if (!isfinite(v)) continue;
+    if (cnt == 0 || v < lo) lo = v;
+    if (cnt == 0 || v > hi) hi = v;
+    cnt++;
+  }
+  *vmin = lo;
+  *vmax = hi;
+  return cnt;
+}
+
+double lopc_ref_noa_eps(const void* x, uint64_t n, int dtype, double rel) {
+  double lo, hi;
+  if (lopc_ref_value_range(x, n, dtype, &lo, &hi) == 0) return rel;
+  double r = hi - lo;
+  return r > 0 ? rel * r : rel;
+}

@@ -92,6 +92,11 @@ uint64_t lopc_ref_order_violations(const void* x, const void* y, int ndims, cons
 /* number of points violating: escaped -> bit-identical; regular ->
  * 0 <= x - y <= eps in exact arithmetic. */
 uint64_t lopc_ref_bound_violations(const void* x, const void* y, uint64_t n, int dtype, double eps);
+/* Row a0 (NOA): min and max over the finite values (as doubles) and
+ * their count; eps = rel * (max - min) computed in double, or rel when there
+ * is no finite value or max == min (the caller's convention). */
+uint64_t lopc_ref_value_range(const void* x, uint64_t n, int dtype, double* vmin, double* vmax);
+double lopc_ref_noa_eps(const void* x, uint64_t n, int dtype, double rel);
 /* Bellman certificate: number of points where s != max(0, max_arcs s(n)+w). */
 uint64_t lopc_ref_certify(const void* x, int ndims, const uint64_t* dims, int dtype, double eps,
                           const uint32_t* s);

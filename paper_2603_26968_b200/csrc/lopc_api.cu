@@ -17,6 +17,8 @@
 #include "../../include/lopc.h"
 #include "lopc_codec.cuh"
 #include "lopc_repair.cuh"
+#include "lopc_noa.cuh"
+#include "lopc_check.cuh"
 
 using namespace lopc;
 
@@ -742,5 +744,118 @@ int lopc_decompress(const void* in, size_t in_bytes, void* out, size_t out_capac
 }
 
 }  // extern "C"
+
+
+// ---- row a0 / NEXT f1: NOA eps on the device -------------------------------
+namespace {
+double host_value_of_key(long long k, int dtype) {
+  if (dtype == LOPC_F32) {
+    const uint32_t b = k >= 0 ? (uint32_t)k : (0x80000000u | (uint32_t)(-k));
+    float f;
+    memcpy(&f, &b, 4);
+    return (double)f;
+  }
+  const uint64_t b = k >= 0 ? (uint64_t)k : (0x8000000000000000ull | (uint64_t)(-k));
+  double d;
+  memcpy(&d, &b, 8);
+  return d;
+}
+}  // namespace
+
+extern "C" {
+
+int lopc_value_range(const void* in, int ndims, const uint64_t* dims, int dtype, double* vmin, double* vmax,
+                     uint64_t* n_finite, void* workspace, size_t workspace_bytes, void* stream) {
+  Shape sh;
+  int rc = make_shape(ndims, dims, dtype, sh);
+  if (rc) return rc;
+  if ((!in && sh.n) || !workspace || workspace_bytes < sizeof(RangeOut)) return !workspace ? LOPC_E_ARG : LOPC_E_NOSPACE;
+  if (sh.n && !is_device_ptr(in)) return LOPC_E_ARG;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  RangeOut h{LLONG_MAX, LLONG_MIN, 0};
+  RangeOut* d = static_cast<RangeOut*>(workspace);
+  CK(cudaMemcpyAsync(d, &h, sizeof(h), cudaMemcpyHostToDevice, st));
+  if (sh.n) {
+    DevInfo* di;
+    if ((rc = dev_info(di))) return rc;
+    uint64_t grid = (sh.n / 4 + 255) / 256;
+    const uint64_t gmax = (uint64_t)di->sms * 8;
+    if (grid > gmax) grid = gmax;
+    if (grid < 1) grid = 1;
+    if (sh.dtype == LOPC_F32)
+      k_value_range<float><<<(unsigned)grid, 256, 0, st>>>(static_cast<const float*>(in), sh.n, d);
+    else
+      k_value_range<double><<<(unsigned)grid, 256, 0, st>>>(static_cast<const double*>(in), sh.n, d);
+    CK(cudaGetLastError());
+  }
+  CK(cudaMemcpyAsync(&h, d, sizeof(h), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (n_finite) *n_finite = h.n_finite;
+  if (vmin) *vmin = h.n_finite ? host_value_of_key(h.kmin, dtype) : 0.0;
+  if (vmax) *vmax = h.n_finite ? host_value_of_key(h.kmax, dtype) : 0.0;
+  return LOPC_OK;
+}
+
+double lopc_noa_eps(double vmin, double vmax, uint64_t n_finite, double rel) {
+  if (!n_finite) return rel;
+  const double r = vmax - vmin;
+  return r > 0 ? rel * r : rel;
+}
+
+int lopc_compress_noa(const void* in, int ndims, const uint64_t* dims, int dtype, double rel, void* out,
+                      size_t* out_bytes, double* eps_used, void* workspace, size_t workspace_bytes, void* stream) {
+  double lo = 0, hi = 0;
+  uint64_t nf = 0;
+  int rc = lopc_value_range(in, ndims, dims, dtype, &lo, &hi, &nf, workspace, workspace_bytes, stream);
+  if (rc) return rc;
+  const double eps = lopc_noa_eps(lo, hi, nf, rel);
+  if (eps_used) *eps_used = eps;
+  return lopc_compress_ex(in, ndims, dims, dtype, eps, out, out_bytes, workspace, workspace_bytes, stream);
+}
+
+}  // extern "C"
+
+
+// ---- k_check: order / bound / error statistics on the device ---------------
+extern "C" int lopc_check(const void* x, const void* y, int ndims, const uint64_t* dims, int dtype, double eps,
+                          lopc_check_result* res, void* workspace, size_t workspace_bytes, void* stream) {
+  Shape sh;
+  int rc = make_shape(ndims, dims, dtype, sh);
+  if (rc) return rc;
+  if (!res || !workspace) return LOPC_E_ARG;
+  if ((rc = check_eps(eps))) return rc;
+  if (workspace_bytes < sizeof(CheckOut)) return LOPC_E_NOSPACE;
+  if (sh.n && (!is_device_ptr(x) || !is_device_ptr(y))) return LOPC_E_ARG;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  CheckOut* d = static_cast<CheckOut*>(workspace);
+  CK(cudaMemsetAsync(d, 0, sizeof(CheckOut), st));
+  if (sh.n) {
+    DevInfo* di;
+    if ((rc = dev_info(di))) return rc;
+    uint64_t grid = (sh.n + 255) / 256;
+    if (grid > (uint64_t)di->sms * 8) grid = (uint64_t)di->sms * 8;
+    const float i32 = inv32_of(eps);
+    const double inv = 1.0 / eps;
+#define KC(TT, ND)                                                                                             \
+  k_check<TT, ND><<<(unsigned)grid, 256, 0, st>>>(static_cast<const TT*>(x), static_cast<const TT*>(y),       \
+                                                   (int64_t)sh.d0, (int64_t)sh.d1, (int64_t)sh.d2, eps, inv, i32, d)
+    if (sh.dtype == LOPC_F32) {
+      if (sh.ndims == 3) KC(float, 3); else KC(float, 2);
+    } else {
+      if (sh.ndims == 3) KC(double, 3); else KC(double, 2);
+    }
+#undef KC
+    CK(cudaGetLastError());
+  }
+  CheckOut h;
+  CK(cudaMemcpyAsync(&h, d, sizeof(h), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  res->order_violations = h.order_bad;
+  res->bound_violations = h.bound_bad;
+  res->n_regular = h.n_regular;
+  memcpy(&res->max_abs_err, &h.max_err_bits, 8);
+  res->sum_sq_err = h.sum_sq;
+  return LOPC_OK;
+}
 
 #include "lopc_slab.cuh"

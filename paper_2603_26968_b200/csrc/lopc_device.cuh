@@ -7,6 +7,7 @@
 // Compiled with -fmad=false: no FMA contraction anywhere; __fma_rn is used
 // explicitly only for the TwoProduct error term of lo().
 #pragma once
+#include <climits>
 #include <cstdint>
 #include <cuda_runtime.h>
 

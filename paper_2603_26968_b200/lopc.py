@@ -345,3 +345,92 @@ def compress_slabs_local(x: torch.Tensor, eps: float, bounds) -> torch.Tensor:
                                          float(eps), len(bounds) - 1, b, C.c_void_p(out.data_ptr()), C.byref(nb))
     _check(rc, "lopc_compress_slabs_local")
     return out[: nb.value]
+
+
+# ---- row a0 / f1: NOA eps on the device -------------------------------------
+def _noa_syms(L):
+    if getattr(L, "_noa_ready", False):
+        return L
+    P, I, D, SZ, U64P = C.c_void_p, C.c_int, C.c_double, C.c_size_t, C.POINTER(C.c_uint64)
+    L.lopc_value_range.argtypes = [P, I, U64P, I, C.POINTER(D), C.POINTER(D), U64P, P, SZ, P]
+    L.lopc_value_range.restype = I
+    L.lopc_noa_eps.argtypes = [D, D, C.c_uint64, D]
+    L.lopc_noa_eps.restype = D
+    L.lopc_compress_noa.argtypes = [P, I, U64P, I, D, P, C.POINTER(SZ), C.POINTER(D), P, SZ, P]
+    L.lopc_compress_noa.restype = I
+    L._noa_ready = True
+    return L
+
+
+def value_range(x: torch.Tensor):
+    """(min, max, finite count) of a device tensor, one fused read (k_value_range)."""
+    L = _noa_syms(load())
+    x = x.contiguous()
+    ws = _workspace(256, x.device)
+    lo, hi, n = C.c_double(), C.c_double(), C.c_uint64()
+    with torch.cuda.device(x.device):
+        rc = L.lopc_value_range(C.c_void_p(x.data_ptr()), x.dim(), _dims(x.shape), _dtype_code(x.dtype),
+                                C.byref(lo), C.byref(hi), C.byref(n), C.c_void_p(ws.data_ptr()), ws.numel(),
+                                _stream(x.device))
+    _check(rc, "lopc_value_range")
+    return lo.value, hi.value, int(n.value)
+
+
+def noa_eps(vmin: float, vmax: float, n_finite: int, rel: float) -> float:
+    return float(_noa_syms(load(False)).lopc_noa_eps(vmin, vmax, n_finite, rel))
+
+
+def compress_noa(x: torch.Tensor, rel: float, out: torch.Tensor | None = None):
+    """lopc_compress_noa: eps = rel * (max - min) found on the device, then
+    compress.  Returns (stream view, eps)."""
+    L = _noa_syms(load())
+    x = x.contiguous()
+    if not x.is_cuda:
+        raise ValueError("compress_noa takes a device tensor")
+    cap = compress_bound(x.shape, x.dtype)
+    if out is None:
+        out = torch.empty(cap, dtype=torch.uint8, device=x.device)
+    need = max(256, L.lopc_compress_workspace_bytes(x.dim(), _dims(x.shape), _dtype_code(x.dtype), 0))
+    ws = _workspace(need, x.device)
+    nb = C.c_size_t(out.numel())
+    e = C.c_double()
+    with torch.cuda.device(x.device):
+        rc = L.lopc_compress_noa(C.c_void_p(x.data_ptr()), x.dim(), _dims(x.shape), _dtype_code(x.dtype), float(rel),
+                                 C.c_void_p(out.data_ptr()), C.byref(nb), C.byref(e), C.c_void_p(ws.data_ptr()),
+                                 ws.numel(), _stream(x.device))
+    _check(rc, "lopc_compress_noa")
+    return out[: nb.value], e.value
+
+
+# ---- k_check: order / bound / error statistics -------------------------------
+class CheckResult(C.Structure):
+    _fields_ = [("order_violations", C.c_uint64), ("bound_violations", C.c_uint64), ("n_regular", C.c_uint64),
+                ("max_abs_err", C.c_double), ("sum_sq_err", C.c_double)]
+
+
+def check(x: torch.Tensor, y: torch.Tensor, eps: float) -> dict:
+    """lopc_check on two device arrays of the same grid; adds mse and PSNR
+    (20 log10(range) - 10 log10(mse), range over the finite values of x)."""
+    import math
+
+    L = _noa_syms(load())
+    if not getattr(L, "_check_ready", False):
+        L.lopc_check.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.POINTER(C.c_uint64), C.c_int, C.c_double,
+                                 C.POINTER(CheckResult), C.c_void_p, C.c_size_t, C.c_void_p]
+        L.lopc_check.restype = C.c_int
+        L._check_ready = True
+    x, y = x.contiguous(), y.contiguous()
+    if x.shape != y.shape or x.dtype != y.dtype:
+        raise ValueError("x and y must have the same shape and dtype")
+    ws = _workspace(256, x.device)
+    r = CheckResult()
+    with torch.cuda.device(x.device):
+        rc = L.lopc_check(C.c_void_p(x.data_ptr()), C.c_void_p(y.data_ptr()), x.dim(), _dims(x.shape),
+                          _dtype_code(x.dtype), float(eps), C.byref(r), C.c_void_p(ws.data_ptr()), ws.numel(),
+                          _stream(x.device))
+    _check(rc, "lopc_check")
+    d = {n: getattr(r, n) for n, _ in CheckResult._fields_}
+    lo, hi, _ = value_range(x)
+    d["mse"] = d["sum_sq_err"] / d["n_regular"] if d["n_regular"] else 0.0
+    d["psnr_db"] = (20 * math.log10(hi - lo) - 10 * math.log10(d["mse"])) if d["mse"] > 0 and hi > lo else None
+    return d
