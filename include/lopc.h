@@ -128,6 +128,13 @@ int lopc_last_stats(lopc_stats* out);
  * records per-phase clocks of the codec kernels (diagnostic, slower). */
 void lopc_set_timing(int enable);
 
+/* Repair schedule (process-wide; NEXT f2 ablation).  0 (default): a dense,
+ * exact tile-local level-set pass then point worklist passes for what crosses
+ * tiles; 1: the paper's point worklist from the first pass (Alg. 2 over every
+ * point, then the points whose inputs rose).  Both reach the same
+ * unique least fixpoint, hence the same bytes.  Slab mode uses engine 0. */
+int lopc_set_repair_engine(int engine);
+
 /* Message for a return code; lopc_last_error_string() adds CUDA detail. */
 const char* lopc_strerror(int code);
 const char* lopc_last_error_string(void);

@@ -27,6 +27,7 @@ namespace {
 char g_errmsg[512] = "";
 lopc_stats g_stats{};
 int g_timing = 0;
+int g_engine = 0;  // lopc_set_repair_engine
 
 int set_cuda_error(cudaError_t e, const char* where) {
   snprintf(g_errmsg, sizeof(g_errmsg), "%s: %s (%s)", where, cudaGetErrorName(e), cudaGetErrorString(e));
@@ -274,6 +275,7 @@ RepairArgs make_repair_args(const Shape& sh, const void* x, double eps, uint8_t*
   ra.own_hi = (int64_t)sh.n;
   ra.skip_dense = 0;
   ra.prof = g_timing >= 2;
+  ra.engine = g_engine;
   return ra;
 }
 
@@ -329,6 +331,7 @@ int run_repair(const Shape& sh, const void* x, double eps, uint8_t* ws, const CL
   RepairArgs ra = make_repair_args(sh, x, eps, ws, L);
   int rc = launch_quant_flags(sh, ra, L, st);
   if (rc) return rc;
+  if (ra.engine) CK(cudaMemsetAsync(ra.s, 0, 4 * sh.n, st));  // the worklist engine starts from s = 0
   tm.mark();
   if ((rc = launch_sweep(sh, ra, L, st))) return rc;
   tm.mark();
@@ -382,6 +385,12 @@ const char* lopc_strerror(int code) {
 const char* lopc_last_error_string(void) { return g_errmsg; }
 
 void lopc_set_timing(int enable) { g_timing = enable; }
+
+int lopc_set_repair_engine(int engine) {
+  if (engine != 0 && engine != 1) return LOPC_E_ARG;
+  g_engine = engine;
+  return LOPC_OK;
+}
 
 int lopc_last_stats(lopc_stats* out) {
   if (!out) return LOPC_E_ARG;

@@ -164,6 +164,7 @@ struct RepairArgs {
   int64_t own_lo, own_hi;  // points with incoming arcs: [own_lo, own_hi) (slab mode; else [0, N))
   int skip_dense;          // k_sweep: start with the sparse passes (slab rounds >= 2)
   int prof;                // diagnostic: k_sweep pass times (ns) into ctr->phase[14..15]
+  int engine;              // 0: dense tile pass + worklist tail; 1: the paper's point worklist from pass 1 (f2)
 };
 
 __device__ __forceinline__ uint64_t gtimer() {
@@ -436,7 +437,7 @@ __global__ void __launch_bounds__(kSweepThreads, 3) k_sweep(RepairArgs a) {
   const uint64_t t_start = (a.prof && tid == 0 && blockIdx.x == 0) ? gtimer() : 0;
   // ---- pass 1: dense, one warp per tile, bit-parallel levels -----------------
   const uint32_t gwarp = blockIdx.x * kSweepWarps + warp, nwarps = gridDim.x * kSweepWarps;
-  const uint32_t ntl = a.skip_dense ? 0u : (uint32_t)a.ntiles;
+  const uint32_t ntl = (a.skip_dense || a.engine) ? 0u : (uint32_t)a.ntiles;
   uint32_t tile = 0;
   if (lane == 0) tile = atomicAdd(&a.ctr->tile_ticket, 1u);
   tile = __shfl_sync(0xffffffffu, tile, 0);
@@ -596,17 +597,20 @@ __global__ void __launch_bounds__(kSweepThreads, 3) k_sweep(RepairArgs a) {
     if (lane == 0) tile = atomicAdd(&a.ctr->tile_ticket, 1u);
     tile = __shfl_sync(0xffffffffu, tile, 0);
   }
-  if (tid == 0 && blockIdx.x == 0 && !a.skip_dense) a.ctr->pass_items[1] = (uint32_t)a.ntiles;
+  if (tid == 0 && blockIdx.x == 0 && !a.skip_dense && !a.engine) a.ctr->pass_items[1] = (uint32_t)a.ntiles;
   grid.sync();
   const uint64_t t_dense = (a.prof && tid == 0 && blockIdx.x == 0) ? gtimer() : 0;
 
   // ---- passes >= 2: sparse, point-level ------------------------------------
   // Whole grid while the list is long; once it is short, block 0 finishes
   // alone with block barriers (no grid-wide barrier per pass).
-  int q = 2;
+  // engine 1 (the paper's schedule): pass 1 visits every point
+  // (s = 0 everywhere), later passes the points whose inputs rose.
+  int q = (a.engine && !a.skip_dense) ? 1 : 2;
   bool small = false;
   for (; q <= a.max_passes; ++q) {
-    const unsigned long long n = *(volatile unsigned long long*)&a.ctr->list_count[q % 3];
+    const unsigned long long n =
+        q == 1 ? (unsigned long long)a.cap : *(volatile unsigned long long*)&a.ctr->list_count[q % 3];
     if (n == 0) break;
     if (!small && n <= kSmallList) {
       small = true;
@@ -622,9 +626,13 @@ __global__ void __launch_bounds__(kSweepThreads, 3) k_sweep(RepairArgs a) {
       uint32_t best = 0;
       bool raised = false;
       if (act) {
-        p = (Idx)__ldcg(&Lq[i]);
-        const uint32_t bit = 1u << ((uint32_t)p & 31u);
-        atomicAnd(&a.bitmap[(size_t)(q & 1) * a.bmw + ((UIdx)p >> 5)], ~bit);
+        if (q == 1) {
+          p = (Idx)i;
+        } else {
+          p = (Idx)__ldcg(&Lq[i]);
+          const uint32_t bit = 1u << ((uint32_t)p & 31u);
+          atomicAnd(&a.bitmap[(size_t)(q & 1) * a.bmw + ((UIdx)p >> 5)], ~bit);
+        }
         z = p / plane;
         const Idx r2 = p - z * plane;
         y = r2 / d2;

@@ -120,6 +120,7 @@ struct Slab {
     ra = make_repair_args(geo.box, xbox(), eps, ws, lay.L);
     ra.own_lo = (int64_t)own_lo();
     ra.own_hi = (int64_t)own_hi();
+    ra.engine = 0;  // slab rounds build on the dense pass
     return LOPC_OK;
   }
   // halo pointers (element size esz: k for x, 4 for s)

@@ -204,6 +204,14 @@ def set_timing(on=True):
     load(False).lopc_set_timing(int(on) if not isinstance(on, bool) else (1 if on else 0))
 
 
+def set_repair_engine(engine: int):
+    """0: dense tile levels + worklist tail (default); 1: the paper's point worklist."""
+    L = load(False)
+    L.lopc_set_repair_engine.argtypes = [C.c_int]
+    L.lopc_set_repair_engine.restype = C.c_int
+    _check(L.lopc_set_repair_engine(int(engine)), "lopc_set_repair_engine")
+
+
 def last_stats() -> dict:
     st = Stats()
     load(False).lopc_last_stats(C.byref(st))
