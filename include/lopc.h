@@ -120,6 +120,7 @@ typedef struct {
   uint64_t phase_cycles[16];  /* diagnostic (lopc_set_timing(2)): SM cycles per codec phase, summed over chunks */
   float ms_place;             /* compress: k_chunk_scan + k_place; decompress: k_chunk_scan */
   uint32_t launches;          /* kernels this library launched in the call */
+  float pass_us[16];          /* diagnostic (lopc_set_timing(2)): k_sweep pass q ended pass_us[q] us after its start */
 } lopc_stats;
 
 int lopc_last_stats(lopc_stats* out);

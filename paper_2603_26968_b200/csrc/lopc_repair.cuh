@@ -68,7 +68,10 @@ constexpr int kSweepThreads = 256;
 constexpr int kSweepWarps = kSweepThreads / 32;
 constexpr int kPassHist = 16;
 constexpr int kLevelPlanes = 8;  // dense-pass levels per tile before handing over to the worklist
-constexpr unsigned long long kSmallList = 256;  // sparse passes this short run on one block
+constexpr unsigned long long kSmallList = 256;
+constexpr int kChase = 8;          // depth-first successor stack per lane in the sparse passes
+constexpr int kChaseBudget = 12;   // chased evaluations per list point
+constexpr unsigned long long kChaseMaxList = 1ull << 18;  // chase only when the pass list is at most this long  // sparse passes this short run on one block
 constexpr int kMaxLevel = (1 << kLevelPlanes) - 1;
 
 // Star slot j (G2): j < D is +e, j >= D is -e, with e = (j mod D) + 1 read
@@ -116,6 +119,7 @@ struct Counters {
   uint32_t pass_items[kPassHist];    // [1] tiles of the dense pass, [q>1] worklist points of pass q
   unsigned long long phase[16];      // diagnostic: SM cycles per codec phase (lopc_set_timing(2))
   unsigned long long ghost_changed;  // slab mode: ghosts raised by the last k_ghost_inject
+  unsigned long long pass_ns[kPassHist];  // diagnostic (prof): k_sweep pass end times, ns after the launch
 };
 
 // Diagnostic phase clock: thread 0 of a block adds the cycles since the last
@@ -192,6 +196,81 @@ __device__ __forceinline__ void enqueue_warp(const RepairArgs& a, Idx q, bool va
   if (lane == 0) base = atomicAdd(&a.ctr->list_count[pass % 3], (unsigned long long)__popc(m));
   base = __shfl_sync(0xffffffffu, base, 0);
   if (fresh) static_cast<UIdx*>(a.plist)[(size_t)(pass & 1) * a.cap + base + __popc(m & ((1u << lane) - 1u))] = (UIdx)q;
+}
+
+template <int NDIM, typename Idx>
+__device__ __forceinline__ Idx slot_goff(int j, Idx plane, Idx d2) {
+  return (Idx)slot_dz<NDIM>(j) * plane + (Idx)slot_dy<NDIM>(j) * d2 + (Idx)slot_dx<NDIM>(j);
+}
+
+// Successors of point p: the slots j whose neighbour q = p + off(j) has an
+// arc from p (q's flag slot opp(j) is set).  All flag loads are independent.
+template <int NDIM, typename Idx>
+__device__ __forceinline__ uint32_t succ_cand(const RepairArgs& a, bool active, Idx z, Idx y, Idx x) {
+  using G = Geo<NDIM>;
+  constexpr int D = G::D;
+  constexpr int SW = G::SW;
+  const Idx d0 = (Idx)a.d0, d1 = (Idx)a.d1, d2 = (Idx)a.d2;
+  const size_t nseg = (size_t)a.nseg;
+  uint32_t w[2 * D];
+  uint32_t inb = 0;
+#pragma unroll
+  for (int j = 0; j < 2 * D; ++j) {
+    const Idx qx = x + slot_dx<NDIM>(j), qy = y + slot_dy<NDIM>(j), qz = z + slot_dz<NDIM>(j);
+    const bool v = active && qx >= 0 && qx < d2 && qy >= 0 && qy < d1 && qz >= 0 && qz < d0;
+    w[j] = v ? __ldg(a.flags + ((size_t)(qz * d1 + qy) * nseg + (size_t)(qx >> 5)) * SW + slot_opp<NDIM>(j)) : 0u;
+    inb |= (uint32_t)v << j;
+  }
+  uint32_t cand = 0;
+#pragma unroll
+  for (int j = 0; j < 2 * D; ++j) {
+    const uint32_t qx = (uint32_t)(x + slot_dx<NDIM>(j));
+    cand |= (((w[j] >> (qx & 31u)) & 1u) & (inb >> j)) << j;
+  }
+  return cand;
+}
+
+// Enqueue the points p + off(j), j in `mask`, for pass `pass`: all bitmap
+// atomics are issued before any result is used, and the warp reserves its
+// list slots with one atomicAdd (warp-collective: all 32 lanes call).
+template <int NDIM, typename Idx>
+__device__ __forceinline__ void enqueue_mask(const RepairArgs& a, Idx p, uint32_t mask, int pass) {
+  using UIdx = typename std::make_unsigned<Idx>::type;
+  constexpr int D = Geo<NDIM>::D;
+  const Idx d2 = (Idx)a.d2, plane = (Idx)a.d1 * d2;
+  uint32_t old[2 * D];
+#pragma unroll
+  for (int j = 0; j < 2 * D; ++j) {
+    old[j] = 0;
+    if ((mask >> j) & 1u) {
+      const Idx q = p + slot_goff<NDIM, Idx>(j, plane, d2);
+      old[j] = atomicOr(&a.bitmap[(size_t)(pass & 1) * a.bmw + ((UIdx)q >> 5)], 1u << ((uint32_t)q & 31u));
+    }
+  }
+  uint32_t fresh = 0;
+#pragma unroll
+  for (int j = 0; j < 2 * D; ++j) {
+    const Idx q = p + slot_goff<NDIM, Idx>(j, plane, d2);
+    fresh |= (((mask >> j) & 1u) & ((~old[j] >> ((uint32_t)q & 31u)) & 1u)) << j;
+  }
+  const int lane = threadIdx.x & 31;
+  const uint32_t c = __popc(fresh);
+  uint32_t incl = c;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += t;
+  }
+  const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
+  if (!tot) return;
+  unsigned long long base = 0;
+  if (lane == 31) base = atomicAdd(&a.ctr->list_count[pass % 3], (unsigned long long)tot);
+  base = __shfl_sync(0xffffffffu, base, 31) + (incl - c);
+  UIdx* L = static_cast<UIdx*>(a.plist) + (size_t)(pass & 1) * a.cap;
+  for (uint32_t m = fresh; m; m &= m - 1) {
+    const int j = __ffs(m) - 1;
+    L[base++] = (UIdx)(p + slot_goff<NDIM, Idx>(j, plane, d2));
+  }
 }
 
 // Rows of the halo box handled per warp, and elements per lane per row.
@@ -365,10 +444,6 @@ __global__ void __launch_bounds__(kRepairThreads, 3) k_quant_flags(RepairArgs a)
 // ---------------------------------------------------------------------------
 // k_sweep
 // ---------------------------------------------------------------------------
-template <int NDIM, typename Idx>
-__device__ __forceinline__ Idx slot_goff(int j, Idx plane, Idx d2) {
-  return (Idx)slot_dz<NDIM>(j) * plane + (Idx)slot_dy<NDIM>(j) * d2 + (Idx)slot_dx<NDIM>(j);
-}
 
 __device__ __forceinline__ uint32_t xshift(uint32_t v, int dx) {
   // value of the neighbour at x + dx, placed at bit x
@@ -600,6 +675,7 @@ __global__ void __launch_bounds__(kSweepThreads, 3) k_sweep(RepairArgs a) {
   if (tid == 0 && blockIdx.x == 0 && !a.skip_dense && !a.engine) a.ctr->pass_items[1] = (uint32_t)a.ntiles;
   grid.sync();
   const uint64_t t_dense = (a.prof && tid == 0 && blockIdx.x == 0) ? gtimer() : 0;
+  if (a.prof && tid == 0 && blockIdx.x == 0) a.ctr->pass_ns[1] = t_dense - t_start;
 
   // ---- passes >= 2: sparse, point-level ------------------------------------
   // Whole grid while the list is long; once it is short, block 0 finishes
@@ -621,58 +697,74 @@ __global__ void __launch_bounds__(kSweepThreads, 3) k_sweep(RepairArgs a) {
     const unsigned long long wstep = small ? (unsigned long long)kSweepThreads : (unsigned long long)nwarps * 32;
     for (unsigned long long ib = wbase; ib < n; ib += wstep) {
       const unsigned long long i = ib + lane;
-      const bool act = i < n;
-      Idx p = 0, z = 0, y = 0, x = 0;
-      uint32_t best = 0;
-      bool raised = false;
-      if (act) {
+      // Each lane evaluates its list point, then chases the successors of
+      // every point it raises depth-first (Gauss-Seidel within the pass);
+      // what does not fit the small stack goes to the next pass's list.
+      Idx cur = 0;
+      bool have = i < n;
+      if (have) {
         if (q == 1) {
-          p = (Idx)i;
+          cur = (Idx)i;
         } else {
-          p = (Idx)__ldcg(&Lq[i]);
-          const uint32_t bit = 1u << ((uint32_t)p & 31u);
-          atomicAnd(&a.bitmap[(size_t)(q & 1) * a.bmw + ((UIdx)p >> 5)], ~bit);
-        }
-        z = p / plane;
-        const Idx r2 = p - z * plane;
-        y = r2 / d2;
-        x = r2 - y * d2;
-        uint32_t fl = point_flags<NDIM>(a.flags + ((size_t)(z * d1 + y) * nseg + (size_t)(x >> 5)) * SW,
-                                        (uint32_t)x & 31u);
-        while (fl) {
-          const int j = __ffs(fl) - 1;
-          fl &= fl - 1;
-          const int e = (j < D ? j : j - D) + 1;
-          const Idx off = (NDIM == 3 ? (Idx)(e >> 2) * plane : (Idx)0) + (Idx)((e >> 1) & 1) * d2 + (Idx)(e & 1);
-          const uint32_t v = j < D ? __ldcg(&a.s[p + off]) + 1u : __ldcg(&a.s[p - off]);
-          best = v > best ? v : best;
-        }
-        if (best > __ldcg(&a.s[p])) {
-          const uint32_t old = atomicMax(&a.s[p], best);
-          raised = old < best;
+          cur = (Idx)__ldcg(&Lq[i]);
+          const uint32_t bit = 1u << ((uint32_t)cur & 31u);
+          atomicAnd(&a.bitmap[(size_t)(q & 1) * a.bmw + ((UIdx)cur >> 5)], ~bit);
         }
       }
-      if (raised) {
-        ++my_raised;
-        my_max = best > my_max ? best : my_max;
-      }
-      if (!__any_sync(0xffffffffu, raised)) continue;
-#pragma unroll
-      for (int j = 0; j < 2 * D; ++j) {
-        const Idx qx = x + slot_dx<NDIM>(j), qy = y + slot_dy<NDIM>(j), qz = z + slot_dz<NDIM>(j);
-        bool v = raised && qx >= 0 && qx < d2 && qy >= 0 && qy < d1 && qz >= 0 && qz < d0;
-        if (v) {
-          const uint32_t w =
-              __ldg(a.flags + ((size_t)(qz * d1 + qy) * nseg + (size_t)(qx >> 5)) * SW + slot_opp<NDIM>(j));
-          v = (w >> ((uint32_t)qx & 31u)) & 1u;
+      Idx stk[kChase];
+      int sp = 0;
+      int budget = n <= kChaseMaxList ? kChaseBudget : 0;  // long lists: plain passes (no redundant chases)
+      while (__any_sync(0xffffffffu, have)) {
+        Idx z = 0, y = 0, x = 0;
+        uint32_t best = 0;
+        bool raised = false;
+        if (have) {
+          z = cur / plane;
+          const Idx r2 = cur - z * plane;
+          y = r2 / d2;
+          x = r2 - y * d2;
+          uint32_t fl = point_flags<NDIM>(a.flags + ((size_t)(z * d1 + y) * nseg + (size_t)(x >> 5)) * SW,
+                                          (uint32_t)x & 31u);
+          while (fl) {
+            const int j = __ffs(fl) - 1;
+            fl &= fl - 1;
+            const int e = (j < D ? j : j - D) + 1;
+            const Idx off = (NDIM == 3 ? (Idx)(e >> 2) * plane : (Idx)0) + (Idx)((e >> 1) & 1) * d2 + (Idx)(e & 1);
+            const uint32_t v = j < D ? __ldcg(&a.s[cur + off]) + 1u : __ldcg(&a.s[cur - off]);
+            best = v > best ? v : best;
+          }
+          if (best > __ldcg(&a.s[cur])) {
+            const uint32_t old = atomicMax(&a.s[cur], best);
+            raised = old < best;
+          }
         }
-        enqueue_warp<Idx>(a, p + slot_goff<NDIM, Idx>(j, plane, d2), v, q + 1);
+        if (raised) {
+          ++my_raised;
+          my_max = best > my_max ? best : my_max;
+        }
+        uint32_t over = 0;
+        if (__any_sync(0xffffffffu, raised)) {
+          const uint32_t cand = succ_cand<NDIM, Idx>(a, raised, z, y, x);
+          for (uint32_t m = cand; m; m &= m - 1) {
+            const int j = __ffs(m) - 1;
+            if (sp < kChase && budget > 0) {
+              stk[sp++] = cur + slot_goff<NDIM, Idx>(j, plane, d2);
+              --budget;
+            } else {
+              over |= 1u << j;
+            }
+          }
+          if (__any_sync(0xffffffffu, over != 0)) enqueue_mask<NDIM, Idx>(a, cur, over, q + 1);
+        }
+        have = sp > 0;
+        if (have) cur = stk[--sp];
       }
     }
     if (tid == 0 && blockIdx.x == 0) {
       a.ctr->list_count[(q + 2) % 3] = 0;
       if (q < kPassHist) a.ctr->pass_items[q] = (uint32_t)n;
       a.ctr->worklist_points += n;
+      if (a.prof && q < kPassHist) a.ctr->pass_ns[q] = gtimer() - t_start;
     }
     if (small) {
       __threadfence();  // the next pass reads the lists and s through L2
@@ -731,16 +823,7 @@ __global__ void __launch_bounds__(256) k_ghost_inject(RepairArgs a, const uint32
       x = r2 - y * d2;
     }
     if (!__any_sync(0xffffffffu, up)) continue;
-#pragma unroll
-    for (int j = 0; j < 2 * D; ++j) {
-      const Idx qx = x + slot_dx<NDIM>(j), qy = y + slot_dy<NDIM>(j), qz = z + slot_dz<NDIM>(j);
-      bool v = up && qx >= 0 && qx < d2 && qy >= 0 && qy < d1 && qz >= 0 && qz < d0;
-      if (v) {
-        const uint32_t w = __ldg(a.flags + ((size_t)(qz * d1 + qy) * nseg + (size_t)(qx >> 5)) * SW + slot_opp<NDIM>(j));
-        v = (w >> ((uint32_t)qx & 31u)) & 1u;
-      }
-      enqueue_warp<Idx>(a, p + slot_goff<NDIM, Idx>(j, plane, d2), v, 2);
-    }
+    enqueue_mask<NDIM, Idx>(a, p, succ_cand<NDIM, Idx>(a, up, z, y, x), 2);
   }
   changed = __reduce_add_sync(0xffffffffu, changed);
   if (lane == 0 && changed) atomicAdd(&a.ctr->ghost_changed, (unsigned long long)changed);

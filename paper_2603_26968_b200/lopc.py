@@ -37,7 +37,7 @@ class Stats(C.Structure):
         ("max_subbin", C.c_uint32), ("timing_valid", C.c_uint32)] + [
         (n, C.c_float) for n in ("ms_h2d", "ms_quant_repair", "ms_sweep", "ms_encode", "ms_decode", "ms_d2h",
                                  "ms_total")] + [("raised", C.c_uint64), ("pass_items", C.c_uint32 * 16), ("phase_cycles", C.c_uint64 * 16),
-        ("ms_place", C.c_float), ("launches", C.c_uint32)]
+        ("ms_place", C.c_float), ("launches", C.c_uint32), ("pass_us", C.c_float * 16)]
 
 
 _lib = None
@@ -218,6 +218,7 @@ def last_stats() -> dict:
     d = {name: getattr(st, name) for name, _ in Stats._fields_}
     d["pass_items"] = [int(v) for v in st.pass_items]
     d["phase_cycles"] = [int(v) for v in st.phase_cycles]
+    d["pass_us"] = [float(v) for v in st.pass_us]
     return d
 
 
