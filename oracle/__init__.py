@@ -294,3 +294,37 @@ def noa_eps(x: np.ndarray, rel: float) -> float:
     """Row a0: eps = rel * (max - min) over the finite values."""
     x = np.ascontiguousarray(x)
     return float(lib().lopc_ref_noa_eps(_ptr(x), x.size, _dt(x), float(rel)))
+
+
+# ---- NEXT f4: multi-core CPU baseline (oracle/lopc_omp.c, OpenMP) ----------
+OMP_SO = os.path.join(_HERE, "liblopc_omp.so")
+_omp = None
+
+
+def build_omp(force: bool = False) -> str:
+    src = os.path.join(_HERE, "lopc_omp.c")
+    deps = [src, SRC, os.path.join(_HERE, "lopc_ref.h")]
+    if force or not os.path.exists(OMP_SO) or os.path.getmtime(OMP_SO) < max(os.path.getmtime(p) for p in deps):
+        subprocess.check_call(["gcc", *CFLAGS, "-fopenmp", "-o", OMP_SO, src, SRC, "-lm"])
+    return OMP_SO
+
+
+def omp_compress(x: np.ndarray, eps: float, threads: int = 0):
+    """(stream bytes, relaxation sweeps): the OpenMP baseline, all cores by default."""
+    global _omp
+    if _omp is None:
+        build_omp()
+        _omp = C.CDLL(OMP_SO)
+        _omp.lopc_omp_compress.argtypes = [C.c_void_p, C.c_int, C.POINTER(C.c_uint64), C.c_int, C.c_double,
+                                           C.c_void_p, C.POINTER(C.c_size_t), C.c_int, C.POINTER(C.c_uint64)]
+        _omp.lopc_omp_compress.restype = C.c_int
+    x = np.ascontiguousarray(x)
+    cap = compress_bound(x.shape, x.dtype)
+    out = C.create_string_buffer(cap)
+    nb = C.c_size_t(cap)
+    sw = C.c_uint64()
+    rc = _omp.lopc_omp_compress(_ptr(x), x.ndim, _dims(x), _dt(x), float(eps), out, C.byref(nb), int(threads),
+                                C.byref(sw))
+    if rc:
+        raise OracleError(rc, "omp_compress")
+    return out.raw[: nb.value], int(sw.value)

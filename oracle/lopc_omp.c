@@ -1,0 +1,144 @@
+/* lopc_omp.c — NEXT f4: the multi-core CPU baseline (OpenMP, blocked), test
+ * and bench infrastructure beside the single-thread oracle.  NOT the product
+ * path.  Same definitions as lopc_ref.c (whose scalar primitives and chunk
+ * encoder it calls): bins by lopc_ref_bin (O5), the least fixpoint by
+ * parallel in-place relaxation sweeps over z-plane / row blocks (the paper's
+ * "OMP" schedule: every point re-evaluated each sweep until no change;
+ * monotone, so any order reaches the unique fixpoint O9), chunks encoded in
+ * parallel by lopc_ref_encode_chunk, payloads placed by one serial scan.
+ * Parity: tests/test_oracle_omp.py requires the oracle's exact bytes. */
+#include <omp.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include "lopc_ref.h"
+
+static uint64_t bits_of(const void* x, uint64_t i, int dtype) {
+  if (dtype == 0) {
+    uint32_t u;
+    memcpy(&u, (const uint8_t*)x + 4 * i, 4);
+    return u;
+  }
+  uint64_t u;
+  memcpy(&u, (const uint8_t*)x + 8 * i, 8);
+  return u;
+}
+
+static double val_of(const void* x, uint64_t i, int dtype) {
+  if (dtype == 0) {
+    float f;
+    memcpy(&f, (const uint8_t*)x + 4 * i, 4);
+    return (double)f;
+  }
+  double d;
+  memcpy(&d, (const uint8_t*)x + 8 * i, 8);
+  return d;
+}
+
+int lopc_omp_compress(const void* x, int ndims, const uint64_t* dims, int dtype, double eps, void* out,
+                      size_t* out_bytes, int threads, uint64_t* sweeps_out) {
+  if (ndims != 2 && ndims != 3) return -2;
+  if (threads > 0) omp_set_num_threads(threads);
+  const int64_t d0 = ndims == 3 ? (int64_t)dims[0] : 1, d1 = (int64_t)dims[ndims - 2], d2 = (int64_t)dims[ndims - 1];
+  const int64_t n = d0 * d1 * d2, plane = d1 * d2;
+  const int k = dtype ? 8 : 4;
+  const uint64_t W = 16384 / k, C = ((uint64_t)n + W - 1) / W;
+  const size_t cap = *out_bytes;
+  int64_t* bin = malloc(sizeof(int64_t) * (n ? n : 1));
+  int64_t* ord = malloc(sizeof(int64_t) * (n ? n : 1));
+  uint32_t* s = calloc(n ? n : 1, 4);
+  uint8_t* chunks = malloc(32768 * (C ? C : 1));
+  uint32_t* sz = malloc(8 * (C ? C : 1));
+  if (!bin || !ord || !s || !chunks || !sz) return -8;
+  /* a1: exact bins (INT64_MIN = escaped) and ord keys */
+#pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < n; i++) {
+    int64_t b;
+    bin[i] = lopc_ref_bin(val_of(x, i, dtype), eps, dtype, &b) ? b : INT64_MIN;
+    ord[i] = lopc_ref_ord(bits_of(x, i, dtype), dtype);
+  }
+  /* star offsets (Kuhn/Freudenthal, G1): e in {0,1}^r \ 0 and -e */
+  int ez[14], ey[14], ex[14], D = ndims == 3 ? 7 : 3;
+  for (int j = 0; j < D; j++) {
+    int e = j + 1;
+    ez[j] = ndims == 3 ? (e >> 2) & 1 : 0;
+    ey[j] = (e >> 1) & 1;
+    ex[j] = e & 1;
+    ez[j + D] = -ez[j];
+    ey[j + D] = -ey[j];
+    ex[j + D] = -ex[j];
+  }
+  /* a2 + a3: in-place relaxation sweeps over blocks of planes (rows in 2D) */
+  uint64_t sweeps = 0;
+  int changed = 1;
+  while (changed) {
+    changed = 0;
+    sweeps++;
+#pragma omp parallel for schedule(static) reduction(| : changed)
+    for (int64_t p = 0; p < n; p++) {
+      if (bin[p] == INT64_MIN) continue;
+      const int64_t z = p / plane, r = p - z * plane, y = r / d2, xx = r - y * d2;
+      uint32_t best = 0;
+      for (int j = 0; j < 2 * D; j++) {
+        const int64_t qz = z + ez[j], qy = y + ey[j], qx = xx + ex[j];
+        if (qz < 0 || qz >= d0 || qy < 0 || qy >= d1 || qx < 0 || qx >= d2) continue;
+        const int64_t q = (qz * d1 + qy) * d2 + qx;
+        if (bin[q] != bin[p]) continue;  /* escaped q: INT64_MIN != regular bin */
+        if (!(ord[q] < ord[p] || (ord[q] == ord[p] && q < p))) continue;
+        const uint32_t v = __atomic_load_n(&s[q], __ATOMIC_RELAXED) + (q > p ? 1u : 0u);
+        best = v > best ? v : best;
+      }
+      if (best > __atomic_load_n(&s[p], __ATOMIC_RELAXED)) {
+        __atomic_store_n(&s[p], best, __ATOMIC_RELAXED);
+        changed = 1;
+      }
+    }
+  }
+  /* a5/a6: chunks in parallel */
+  int bad = 0;
+#pragma omp parallel for schedule(dynamic, 4) reduction(| : bad)
+  for (int64_t c = 0; c < (int64_t)C; c++)
+    if (lopc_ref_encode_chunk(x, (uint64_t)n, dtype, eps, s, (uint64_t)c, chunks + 32768 * c, sz + 2 * c)) bad = 1;
+  /* a7: header, table, payloads */
+  uint64_t total = 64 + 8 * C;
+  for (uint64_t c = 0; c < C; c++) total += (uint64_t)sz[2 * c] + sz[2 * c + 1];
+  int rc = 0;
+  if (bad) {
+    rc = -8;
+  } else if (total > cap) {
+    rc = -3;
+  } else {
+    uint8_t* o = out;
+    memset(o, 0, 64);
+    memcpy(o, "LOPC", 4);
+    const uint16_t ver = 1;
+    memcpy(o + 4, &ver, 2);
+    o[6] = (uint8_t)dtype;
+    o[7] = (uint8_t)ndims;
+    const uint64_t d3[3] = {(uint64_t)d0, (uint64_t)d1, (uint64_t)d2};
+    memcpy(o + 8, d3, 24);
+    memcpy(o + 32, &eps, 8);
+    const uint64_t nn = (uint64_t)n;
+    memcpy(o + 40, &nn, 8);
+    const uint32_t cb = 16384, c32 = (uint32_t)C;
+    memcpy(o + 48, &cb, 4);
+    memcpy(o + 52, &c32, 4);
+    memcpy(o + 56, &total, 8);
+    memcpy(o + 64, sz, 8 * C);
+    uint64_t off = 64 + 8 * C;
+    for (uint64_t c = 0; c < C; c++) {
+      const uint64_t len = (uint64_t)sz[2 * c] + sz[2 * c + 1];
+      memcpy(o + off, chunks + 32768 * c, len);
+      off += len;
+    }
+  }
+  *out_bytes = total;
+  if (sweeps_out) *sweeps_out = sweeps;
+  free(bin);
+  free(ord);
+  free(s);
+  free(chunks);
+  free(sz);
+  return rc;
+}
