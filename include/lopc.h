@@ -159,6 +159,25 @@ typedef struct {
 int lopc_check(const void* x, const void* y, int ndims, const uint64_t* dims, int dtype, double eps,
                lopc_check_result* res, void* workspace, size_t workspace_bytes, void* stream);
 
+/* Critical-point preservation (NEXT f3; Table III semantics): PL
+ * critical points of x and y under SoS on the Freudenthal triangulation
+ * (lower link empty = minimum, upper empty = maximum, one component each =
+ * regular, else saddle; G5, G27).  false_positives: regular in x, critical in
+ * y; false_negatives: the reverse; false_types: critical in both with
+ * different types; pair_mismatches: (#lower, #upper) link components differ.
+ * Vertices where x is NaN are skipped and NaN neighbours leave the link.
+ * Device arrays; first 256 bytes of workspace. */
+typedef struct {
+  uint64_t false_positives;
+  uint64_t false_negatives;
+  uint64_t false_types;
+  uint64_t pair_mismatches;
+  uint64_t critical_x;
+  uint64_t critical_y;
+} lopc_critical_result;
+int lopc_critical_points(const void* x, const void* y, int ndims, const uint64_t* dims, int dtype,
+                         lopc_critical_result* res, void* workspace, size_t workspace_bytes, void* stream);
+
 /* ---- NOA error bound on the device (row a0) ---------------
  * lopc_value_range: min and max over the finite values of x (device pointer,
  * one read pass; NaN and +-Inf skipped), returned as doubles, and their count.

@@ -868,4 +868,75 @@ extern "C" int lopc_check(const void* x, const void* y, int ndims, const uint64_
   return LOPC_OK;
 }
 
+
+// ---- k_critical: critical-point preservation (Table III) on the device -----
+namespace {
+// Link adjacency of the Freudenthal star: slots i, j are joined iff their
+// offsets differ by a star offset (then {p, p+o_i, p+o_j} is a triangle).
+LinkAdj link_adj(int ndims) {
+  LinkAdj L{};
+  const int D = ndims == 3 ? 7 : 3;
+  int o[14][3];
+  for (int j = 0; j < 2 * D; ++j) {
+    const int e = (j < D ? j : j - D) + 1, sg = j < D ? 1 : -1;
+    o[j][0] = ndims == 3 ? sg * ((e >> 2) & 1) : 0;
+    o[j][1] = sg * ((e >> 1) & 1);
+    o[j][2] = sg * (e & 1);
+  }
+  for (int i = 0; i < 2 * D; ++i)
+    for (int j = 0; j < 2 * D; ++j) {
+      if (i == j) continue;
+      bool pos = true, neg = true, nz = false;
+      for (int c = 0; c < 3; ++c) {
+        const int d = o[j][c] - o[i][c];
+        pos = pos && (d == 0 || d == 1);
+        neg = neg && (d == 0 || d == -1);
+        nz = nz || d != 0;
+      }
+      if (nz && (pos || neg)) L.adj[i] |= (uint16_t)(1u << j);
+    }
+  return L;
+}
+}  // namespace
+
+extern "C" int lopc_critical_points(const void* x, const void* y, int ndims, const uint64_t* dims, int dtype,
+                                    lopc_critical_result* res, void* workspace, size_t workspace_bytes, void* stream) {
+  Shape sh;
+  int rc = make_shape(ndims, dims, dtype, sh);
+  if (rc) return rc;
+  if (!res || !workspace) return LOPC_E_ARG;
+  if (workspace_bytes < sizeof(CritOut)) return LOPC_E_NOSPACE;
+  if (sh.n && (!is_device_ptr(x) || !is_device_ptr(y))) return LOPC_E_ARG;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  CritOut* d = static_cast<CritOut*>(workspace);
+  CK(cudaMemsetAsync(d, 0, sizeof(CritOut), st));
+  if (sh.n) {
+    DevInfo* di;
+    if ((rc = dev_info(di))) return rc;
+    uint64_t grid = (sh.n + 255) / 256;
+    if (grid > (uint64_t)di->sms * 8) grid = (uint64_t)di->sms * 8;
+    const LinkAdj L = link_adj(sh.ndims);
+#define KR(TT, ND)                                                                                          \
+  k_critical<TT, ND><<<(unsigned)grid, 256, 0, st>>>(static_cast<const TT*>(x), static_cast<const TT*>(y), \
+                                                      (int64_t)sh.d0, (int64_t)sh.d1, (int64_t)sh.d2, L, d)
+    if (sh.dtype == LOPC_F32) {
+      if (sh.ndims == 3) KR(float, 3); else KR(float, 2);
+    } else {
+      if (sh.ndims == 3) KR(double, 3); else KR(double, 2);
+    }
+#undef KR
+    CK(cudaGetLastError());
+  }
+  CritOut h;
+  CK(cudaMemcpyAsync(&h, d, sizeof(h), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  res->false_positives = h.fp;
+  res->false_negatives = h.fn;
+  res->false_types = h.ft;
+  res->pair_mismatches = h.pair_bad;
+  res->critical_x = h.crit_x;
+  res->critical_y = h.crit_y;
+  return LOPC_OK;
+}
+
 #include "lopc_slab.cuh"

@@ -79,3 +79,98 @@ __global__ void __launch_bounds__(256) k_check(const T* __restrict__ x, const T*
 }
 
 }  // namespace lopc
+
+namespace lopc {
+
+// ---------------------------------------------------------------------------
+// k_critical: PL critical points of x and x^ under SoS (G5: an empty
+// lower link is a minimum) on the Kuhn/Freudenthal triangulation, and the
+// Table III comparison: false positives / negatives / types, plus the
+// stronger (#lower, #upper link components) mismatch count (G27).  The link
+// of p is its star neighbours joined by the link edges (adj: for each slot,
+// the slots whose offsets differ by a star offset = the triangles through p,
+// 6 edges in 2D, 36 in 3D); out-of-grid and NaN neighbours drop out.
+// ---------------------------------------------------------------------------
+struct CritOut {
+  unsigned long long fp, fn, ft, pair_bad, crit_x, crit_y;
+};
+struct LinkAdj {
+  uint16_t adj[14];
+};
+
+__device__ __forceinline__ int link_components(uint32_t m, const LinkAdj& L) {
+  int c = 0;
+  while (m) {
+    uint32_t comp = m & (0u - m), prev = 0;
+    while (comp != prev) {
+      prev = comp;
+      uint32_t g = comp;
+      for (uint32_t t = comp; t; t &= t - 1) g |= L.adj[__ffs(t) - 1];
+      comp = g & m;
+    }
+    m &= ~comp;
+    ++c;
+  }
+  return c;
+}
+
+// type: 0 regular, 1 min, 2 max, 3 saddle
+__device__ __forceinline__ int crit_type(int nl, int nu) {
+  return nl == 0 ? 1 : (nu == 0 ? 2 : ((nl == 1 && nu == 1) ? 0 : 3));
+}
+
+template <typename T, int NDIM>
+__global__ void __launch_bounds__(256) k_critical(const T* __restrict__ x, const T* __restrict__ y, int64_t d0,
+                                                  int64_t d1, int64_t d2, LinkAdj L, CritOut* out) {
+  constexpr int D = Geo<NDIM>::D;
+  const int64_t plane = d1 * d2, n = d0 * plane;
+  unsigned long long fp = 0, fn = 0, ft = 0, pb = 0, cx = 0, cy = 0;
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
+    const T xp = x[p], yp = y[p];
+    if (xp != xp) continue;
+    const int64_t z = p / plane, r2 = p - z * plane, yy = r2 / d2, xx = r2 - yy * d2;
+    uint32_t in = 0, lx = 0, ly = 0;
+#pragma unroll
+    for (int j = 0; j < 2 * D; ++j) {
+      const int e = (j < D ? j : j - D) + 1, sg = j < D ? 1 : -1;
+      const int dz = NDIM == 3 ? sg * ((e >> 2) & 1) : 0, dy = sg * ((e >> 1) & 1), dx = sg * (e & 1);
+      const int64_t qz = z + dz, qy = yy + dy, qx = xx + dx;
+      if (qz < 0 || qz >= d0 || qy < 0 || qy >= d1 || qx < 0 || qx >= d2) continue;
+      const int64_t q = p + dz * plane + dy * d2 + dx;
+      const T xq = x[q], yq = y[q];
+      if (xq != xq) continue;
+      in |= 1u << j;
+      // SoS: q below p iff smaller value, or equal value and smaller index
+      lx |= (uint32_t)(xq < xp || (xq == xp && q < p)) << j;
+      ly |= (uint32_t)(yq < yp || (yq == yp && q < p)) << j;
+    }
+    const int nlx = link_components(lx, L), nux = link_components(in & ~lx, L);
+    const int nly = link_components(ly, L), nuy = link_components(in & ~ly, L);
+    const int tx = crit_type(nlx, nux), ty = crit_type(nly, nuy);
+    cx += tx != 0;
+    cy += ty != 0;
+    fp += tx == 0 && ty != 0;
+    fn += tx != 0 && ty == 0;
+    ft += tx != 0 && ty != 0 && tx != ty;
+    pb += nlx != nly || nux != nuy;
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    fp += __shfl_xor_sync(0xffffffffu, fp, o);
+    fn += __shfl_xor_sync(0xffffffffu, fn, o);
+    ft += __shfl_xor_sync(0xffffffffu, ft, o);
+    pb += __shfl_xor_sync(0xffffffffu, pb, o);
+    cx += __shfl_xor_sync(0xffffffffu, cx, o);
+    cy += __shfl_xor_sync(0xffffffffu, cy, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (fp) atomicAdd(&out->fp, fp);
+    if (fn) atomicAdd(&out->fn, fn);
+    if (ft) atomicAdd(&out->ft, ft);
+    if (pb) atomicAdd(&out->pair_bad, pb);
+    if (cx) atomicAdd(&out->crit_x, cx);
+    if (cy) atomicAdd(&out->crit_y, cy);
+  }
+}
+
+}  // namespace lopc

@@ -443,3 +443,27 @@ def check(x: torch.Tensor, y: torch.Tensor, eps: float) -> dict:
     d["mse"] = d["sum_sq_err"] / d["n_regular"] if d["n_regular"] else 0.0
     d["psnr_db"] = (20 * math.log10(hi - lo) - 10 * math.log10(d["mse"])) if d["mse"] > 0 and hi > lo else None
     return d
+
+
+class CriticalResult(C.Structure):
+    _fields_ = [(n, C.c_uint64) for n in ("false_positives", "false_negatives", "false_types", "pair_mismatches",
+                                          "critical_x", "critical_y")]
+
+
+def critical_points(x: torch.Tensor, y: torch.Tensor) -> dict:
+    """lopc_critical_points: Table III FP/FN/FT of y against x (device arrays)."""
+    L = load()
+    if not getattr(L, "_crit_ready", False):
+        L.lopc_critical_points.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.POINTER(C.c_uint64), C.c_int,
+                                           C.POINTER(CriticalResult), C.c_void_p, C.c_size_t, C.c_void_p]
+        L.lopc_critical_points.restype = C.c_int
+        L._crit_ready = True
+    x, y = x.contiguous(), y.contiguous()
+    ws = _workspace(256, x.device)
+    r = CriticalResult()
+    with torch.cuda.device(x.device):
+        rc = L.lopc_critical_points(C.c_void_p(x.data_ptr()), C.c_void_p(y.data_ptr()), x.dim(), _dims(x.shape),
+                                    _dtype_code(x.dtype), C.byref(r), C.c_void_p(ws.data_ptr()), ws.numel(),
+                                    _stream(x.device))
+    _check(rc, "lopc_critical_points")
+    return {n: int(getattr(r, n)) for n, _ in CriticalResult._fields_}

@@ -51,13 +51,17 @@ def main():
             y = torch.empty_like(x)
             td, _ = timed(lambda: lopc.decompress(st, out=y))
             chk = lopc.check(x, y, eps)
+            cp = lopc.critical_points(x, y)
             row = {"config": name, "rel": rel, "eps": eps, "compress_ms": tc, "decompress_ms": td,
                    "compress_GBps": raw / tc / 1e6, "decompress_GBps": raw / td / 1e6,
                    "ratio": raw / st.numel(), "bin_bytes": s["bin_bytes"], "sub_bytes": s["sub_bytes"],
                    "sweep_passes": s["sweep_passes"], "worklist_points": s["worklist_points"],
                    "max_subbin": s["max_subbin"], "escapes": s["escapes"],
                    "max_abs_err_over_eps": chk["max_abs_err"] / eps, "psnr_db": chk["psnr_db"],
-                   "order_violations": chk["order_violations"], "bound_violations": chk["bound_violations"]}
+                   "order_violations": chk["order_violations"], "bound_violations": chk["bound_violations"],
+                   "critical_points": cp["critical_x"], "fp_fn_ft": [cp["false_positives"], cp["false_negatives"],
+                                                                     cp["false_types"]],
+                   "pair_mismatches": cp["pair_mismatches"]}
             out["sweep"].append(row)
             print(json.dumps(row), flush=True)
             if rel in (1e-2, 1e-3, 1e-4) and name in ("cfg2", "cfg4"):
