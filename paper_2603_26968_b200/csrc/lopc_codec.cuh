@@ -257,37 +257,56 @@ __device__ uint32_t rze_enc(const uint8_t* in, uint32_t L, int g, uint8_t* out, 
   __syncthreads();
   const uint32_t koff = R.info[0], doff = R.info[1], total = R.info[2];
   if (total <= limit) {
+    const int lane = tid & 31;
 #pragma unroll
     for (int it = 0; it < MAXIT; ++it) {
       if (it >= iters) break;
       const uint32_t u = (uint32_t)(it * kCodecThreads + tid);
-      if (u >= units) continue;
-      const uint32_t m = mk[it] & 0xffffu, b1 = mk[it] >> 16;
-      uint32_t dr = rk[it] & 0xfffffu;
-      const uint32_t kr = rk[it] >> 20;
-      if (top == 0) {  // B0 itself is the top level (<= 8 bytes)
-        if (2 * u < sz[0]) out[2 * u] = (uint8_t)(m & 0xffu);
-        if (2 * u + 1 < sz[0]) out[2 * u + 1] = (uint8_t)(m >> 8);
-      } else {
-        uint32_t k = koff + kr;
-        if (b1 & 1u) out[k++] = (uint8_t)(m & 0xffu);
-        if (b1 & 2u) out[k] = (uint8_t)(m >> 8);
+      const bool valid = u < units;
+      const uint32_t m = valid ? mk[it] & 0xffffu : 0u, b1 = mk[it] >> 16;
+      const uint32_t dr = rk[it] & 0xfffffu;
+      if (valid) {
+        const uint32_t kr = rk[it] >> 20;
+        if (top == 0) {  // B0 itself is the top level (<= 8 bytes)
+          if (2 * u < sz[0]) out[2 * u] = (uint8_t)(m & 0xffu);
+          if (2 * u + 1 < sz[0]) out[2 * u + 1] = (uint8_t)(m >> 8);
+        } else {
+          uint32_t k = koff + kr;
+          if (b1 & 1u) out[k++] = (uint8_t)(m & 0xffu);
+          if (b1 & 2u) out[k] = (uint8_t)(m >> 8);
+        }
       }
-      const uint8_t* p = in + u * ub;
       uint8_t* d = out + doff;
       if (g == 1) {
-        const uint4 v = *reinterpret_cast<const uint4*>(p);
-        const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
+        if (valid) {
+          const uint4 v = *reinterpret_cast<const uint4*>(in + u * ub);
+          const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
+          uint32_t r = dr;
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          if ((m >> j) & 1u) d[dr++] = (uint8_t)(w4[j >> 2] >> (8 * (j & 3)));
+          for (int j = 0; j < 16; ++j) {
+            if ((m >> j) & 1u) d[r++] = (uint8_t)(w4[j >> 2] >> (8 * (j & 3)));
+          }
         }
       } else {
-#pragma unroll 4
-        for (int j = 0; j < 16; ++j) {
-          if ((m >> j) & 1u) {
-            for (int q = 0; q < g; ++q) d[(size_t)dr * g + q] = p[j * g + q];
-            ++dr;
+        // g = 4 / 8: one unit at a time per warp (units with data only), its
+        // 16 g-byte words spread over the lanes: conflict-free reads
+        const int uwl = g == 4 ? 0 : 1;  // log2(u32 per word)
+        const int pu = 16 << uwl;         // u32 per unit
+        const uint32_t* in32 = reinterpret_cast<const uint32_t*>(in);
+        for (uint32_t nzl = __ballot_sync(0xffffffffu, m != 0); nzl; nzl &= nzl - 1) {
+          const int l = __ffs(nzl) - 1;
+          const uint32_t mu = __shfl_sync(0xffffffffu, m, l), du = __shfl_sync(0xffffffffu, dr, l);
+          const uint32_t uu = u - lane + l;
+          if (lane < pu) {
+            const int j = lane >> uwl, hh = lane & ((1 << uwl) - 1);
+            if ((mu >> j) & 1u) {
+              const uint32_t w = in32[uu * pu + lane];
+              uint8_t* o = d + (size_t)(du + __popc(mu & ((1u << j) - 1u))) * g + 4 * hh;
+              o[0] = (uint8_t)w;
+              o[1] = (uint8_t)(w >> 8);
+              o[2] = (uint8_t)(w >> 16);
+              o[3] = (uint8_t)(w >> 24);
+            }
           }
         }
       }
@@ -307,6 +326,10 @@ __device__ uint32_t rze_dec(const uint8_t* in, uint32_t in_len, uint32_t L, int 
   uint32_t sz[6];
   const int top = rze_sizes(n, sz);
   const uint32_t units = (n + 15) / 16, ub = 16u * (uint32_t)g;
+  if (g != 1) {  // words without data stay 0 (the scatter below writes only the others)
+    uint4* o4 = reinterpret_cast<uint4*>(out);
+    for (uint32_t t = tid; t < units * ub / 16; t += kCodecThreads) o4[t] = make_uint4(0, 0, 0, 0);
+  }
   if (tid < 32) {
     const int lane = tid;
     bool ok = sz[top] <= in_len;
@@ -397,28 +420,34 @@ __device__ uint32_t rze_dec(const uint8_t* in, uint32_t in_len, uint32_t L, int 
     uint32_t dr = running + block_scan_excl<uint32_t>((uint32_t)__popc(m), R.wsum, &tot);
     running += tot;
     if (doff + (uint32_t)g * running > in_len) bad = true;  // block-uniform
-    if (!bad && u < units) {
+    if (!bad && g == 1 && u < units) {
       const uint8_t* src = in + doff;
       uint8_t* dst = out + u * ub;
-      if (g == 1) {
-        uint32_t w4[4] = {0, 0, 0, 0};
+      uint32_t w4[4] = {0, 0, 0, 0};
 #pragma unroll
-        for (int j = 0; j < 16; ++j)
-          if ((m >> j) & 1u) w4[j >> 2] |= (uint32_t)src[dr++] << (8 * (j & 3));
-        *reinterpret_cast<uint4*>(dst) = make_uint4(w4[0], w4[1], w4[2], w4[3]);
-      } else {
-        uint32_t* d32 = reinterpret_cast<uint32_t*>(dst);
-#pragma unroll 4
-        for (int j = 0; j < 16; ++j) {
-          for (int q = 0; q < g / 4; ++q) {
-            uint32_t v = 0;
-            if ((m >> j) & 1u) {
-              const uint8_t* b = src + (size_t)dr * g + 4 * q;
-              v = (uint32_t)b[0] | ((uint32_t)b[1] << 8) | ((uint32_t)b[2] << 16) | ((uint32_t)b[3] << 24);
-            }
-            d32[j * (g / 4) + q] = v;
+      for (int j = 0; j < 16; ++j)
+        if ((m >> j) & 1u) w4[j >> 2] |= (uint32_t)src[dr++] << (8 * (j & 3));
+      *reinterpret_cast<uint4*>(dst) = make_uint4(w4[0], w4[1], w4[2], w4[3]);
+    } else if (!bad && g != 1) {
+      // g = 4 / 8: `out` was zeroed up front; units with data are written one
+      // at a time per warp, their words spread over the lanes (conflict-free)
+      const int lane = tid & 31;
+      const int uwl = g == 4 ? 0 : 1;
+      const int pu = 16 << uwl;
+      const uint8_t* src = in + doff;
+      uint32_t* out32 = reinterpret_cast<uint32_t*>(out);
+      const uint32_t mm = u < units ? m : 0u;
+      for (uint32_t nzl = __ballot_sync(0xffffffffu, mm != 0); nzl; nzl &= nzl - 1) {
+        const int l = __ffs(nzl) - 1;
+        const uint32_t mu = __shfl_sync(0xffffffffu, mm, l), du = __shfl_sync(0xffffffffu, dr, l);
+        const uint32_t uu = u - lane + l;
+        if (lane < pu) {
+          const int j = lane >> uwl, hh = lane & ((1 << uwl) - 1);
+          if ((mu >> j) & 1u) {
+            const uint8_t* b = src + (size_t)(du + __popc(mu & ((1u << j) - 1u))) * g + 4 * hh;
+            out32[uu * pu + lane] =
+                (uint32_t)b[0] | ((uint32_t)b[1] << 8) | ((uint32_t)b[2] << 16) | ((uint32_t)b[3] << 24);
           }
-          dr += (m >> j) & 1u;
         }
       }
     }
@@ -1109,39 +1138,58 @@ __device__ __noinline__ void decode_stream(const DecodeArgs& a, const uint8_t* p
 
 // a8: x^ = value with key(lo(b)) + s, or the raw escape (G10), for the
 // half `r` of chunk c; WB/WS point at the two CTAs' word buffers (DSMEM).
+// Thread t owns PER consecutive elements: lo(b) is computed only when the
+// bin changes from the thread's previous element (bins are locally
+// repetitive), and the values leave as 16-byte stores.
 template <typename T>
 __device__ __forceinline__ void reconstruct_half(const DecodeArgs& a, const Hdr& h, uint32_t c, int r, const uint8_t* wb,
-                                                 const uint8_t* ws) {
+                                                 int wb_off, const uint8_t* ws, int ws_off) {
   using U = typename VT<T>::U;
   using I = typename VT<T>::I;
   constexpr int W = kChunkBytes / VT<T>::K;
-  constexpr int PER = W / kCodecThreads / 2;
+  constexpr int PER = W / kCodecThreads / 2;  // 8 (f32) / 4 (f64)
   const U* WB = reinterpret_cast<const U*>(wb);
   const U* SW = reinterpret_cast<const U*>(ws);
   const uint64_t e0 = (uint64_t)c * W;
   const uint32_t cnt = (uint32_t)min((uint64_t)W, h.n - e0);
-  T* O = static_cast<T*>(a.out) + e0;
+  const int i0 = r * (W / 2) + threadIdx.x * PER;
+  U bwv[PER], swv[PER];
 #pragma unroll
   for (int v = 0; v < PER; ++v) {
-    const int i = (2 * v + r) * kCodecThreads + threadIdx.x;
-    if ((uint32_t)i < cnt) {
-      const U bw = WB[swz(i)], sw = SW[swz(i)];
-      U bits;
-      if (bw == VT<T>::kSentinel) {
-        bits = sw;
-      } else {
-        const T lo = lo_t<T>((int64_t)(I)bw, h.eps);
-        const int64_t k = (int64_t)key_of((U)as_bits(lo)) + (int64_t)sw;
-        if constexpr (sizeof(U) == 4)
-          bits = bits_of_key32(k);
-        else
-          bits = bits_of_key64(k);
-      }
-      if constexpr (sizeof(U) == 4)
-        __stcs(&O[i], __uint_as_float(bits));
-      else
-        __stcs(&O[i], __longlong_as_double((long long)bits));
+    bwv[v] = WB[swz(i0 + v - wb_off)];
+    swv[v] = SW[swz(i0 + v - ws_off)];
+  }
+  U out[PER];
+  U pb = VT<T>::kSentinel;
+  int64_t pk = 0;
+#pragma unroll
+  for (int v = 0; v < PER; ++v) {
+    const U bw = bwv[v];
+    if (bw != pb && bw != VT<T>::kSentinel) {
+      pk = (int64_t)key_of((U)as_bits(lo_t<T>((int64_t)(I)bw, h.eps)));
+      pb = bw;
     }
+    const int64_t k = pk + (int64_t)swv[v];
+    U bits;
+    if constexpr (sizeof(U) == 4)
+      bits = bits_of_key32(k);
+    else
+      bits = bits_of_key64(k);
+    out[v] = bw == VT<T>::kSentinel ? swv[v] : bits;
+  }
+  T* O = static_cast<T*>(a.out) + e0 + i0;
+  if ((uint32_t)i0 + PER <= cnt && ((uintptr_t)O & 15) == 0) {
+#pragma unroll
+    for (int v = 0; v < PER; v += 16 / (int)sizeof(T)) {
+      if constexpr (sizeof(T) == 4)
+        __stcs(reinterpret_cast<uint4*>(O + v), make_uint4(out[v], out[v + 1], out[v + 2], out[v + 3]));
+      else
+        __stcs(reinterpret_cast<ulonglong2*>(O + v), make_ulonglong2(out[v], out[v + 1]));
+    }
+  } else {
+#pragma unroll
+    for (int v = 0; v < PER; ++v)
+      if ((uint32_t)(i0 + v) < cnt) reinterpret_cast<U*>(O)[v] = out[v];
   }
 }
 
@@ -1188,11 +1236,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kCodecThreads, 4) k_
       decode_stream<double>(a, p, sz, r != 0, sm);
     cl.sync();
     const uint64_t c = a.c_begin + l;
-    if (!s0->bad && !s1->bad) {
+    const bool ok = !s0->bad && !s1->bad;
+    // the partner's words of this CTA's half, copied once into local smem
+    // with 16-byte DSMEM loads (sm.O is free here)
+    constexpr int HB = kChunkBytes / 2;
+    if (ok) {
+      const uint4* rem = reinterpret_cast<const uint4*>((r ? s0->Wd : s1->Wd) + r * HB);
+      uint4* loc = reinterpret_cast<uint4*>(sm.O);
+      for (int t = tid; t < HB / 16; t += kCodecThreads) loc[t] = rem[t];
+    }
+    cl.sync();  // remote reads done (the partner may overwrite its words next); local copy visible
+    if (ok) {
+      const int half_w = h.dtype == 0 ? 2048 : 1024;  // W / 2
+      const uint8_t* own = sm.Wd;
       if (h.dtype == 0)
-        reconstruct_half<float>(a, h, (uint32_t)c, r, s0->Wd, s1->Wd);
+        reconstruct_half<float>(a, h, (uint32_t)c, r, r ? sm.O : own, r ? half_w : 0, r ? own : sm.O,
+                                r ? 0 : half_w * 0);
       else
-        reconstruct_half<double>(a, h, (uint32_t)c, r, s0->Wd, s1->Wd);
+        reconstruct_half<double>(a, h, (uint32_t)c, r, r ? sm.O : own, r ? half_w : 0, r ? own : sm.O,
+                                 r ? 0 : half_w * 0);
     }
   }
 }
