@@ -598,6 +598,7 @@ struct EncodeArgs {
   float inv32;  // RN32(1/eps) for the f32 fast path, NaN = off
   int prof;     // diagnostic phase clocks
   uint64_t d0, d1, d2;
+  int role;     // 0: both streams (grid 2C); 1: bin CTAs only (grid C); 2: subbin CTAs only (grid C)
 };
 
 
@@ -658,8 +659,8 @@ __global__ void __launch_bounds__(kCodecThreads, 5) k_encode(EncodeArgs a) {
   U* WD = reinterpret_cast<U*>(sm.Wd);
   uint16_t* Q = reinterpret_cast<uint16_t*>(sm.O);
   const int tid = threadIdx.x, lane = tid & 31;
-  const uint32_t c = blockIdx.x >> 1;
-  const bool subs = blockIdx.x & 1;
+  const uint32_t c = a.role ? blockIdx.x : blockIdx.x >> 1;
+  const bool subs = a.role ? a.role == 2 : (blockIdx.x & 1);
   PhaseClock pc;
   pc.start(a.prof);
   if (tid == 0) sm.misc[0] = 0;  // a4 queue length
