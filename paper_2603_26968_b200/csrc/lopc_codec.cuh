@@ -769,8 +769,7 @@ __global__ void __launch_bounds__(kCodecThreads, 5) k_encode(EncodeArgs a) {
       I b = 0;
       if (!qtry(x, a.inv32, a.inv, b)) b = (I)quantize_slow<T>(x, a.eps, a.inv);
       const uint32_t sq = (uint32_t)WD[swz(i)];
-      const T lo = lo_t<T>((int64_t)b, a.eps);
-      if ((int64_t)key_of((U)as_bits(lo)) + (int64_t)sq > (int64_t)key_of((U)as_bits(x))) bad = 1;
+      if ((int64_t)lo_key<T>((int64_t)b, a.eps) + (int64_t)sq > (int64_t)key_of((U)as_bits(x))) bad = 1;
     }
     if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(&a.ctr->err, kErrBound);
     pc.mark(a.ctr, 2);
@@ -1167,7 +1166,7 @@ __device__ __forceinline__ void reconstruct_half(const DecodeArgs& a, const Hdr&
   for (int v = 0; v < PER; ++v) {
     const U bw = bwv[v];
     if (bw != pb && bw != VT<T>::kSentinel) {
-      pk = (int64_t)key_of((U)as_bits(lo_t<T>((int64_t)(I)bw, h.eps)));
+      pk = (int64_t)lo_key<T>((int64_t)(I)bw, h.eps);
       pb = bw;
     }
     const int64_t k = pk + (int64_t)swv[v];

@@ -111,6 +111,28 @@ __device__ __forceinline__ float lo_t<float>(int64_t b, double eps) { return lo_
 template <>
 __device__ __forceinline__ double lo_t<double>(int64_t b, double eps) { return lo_f64(b, eps); }
 
+// key(lo(b)) directly (the only form the kernels need): the same rounding as
+// lo_f32 / lo_f64, with the rare exact-product check off the common path.
+__device__ __forceinline__ int32_t lo_key32(int64_t b, double eps) {
+  const double a = i64_to_f64_exact(b) - 0.5;
+  const double p = __dmul_rn(a, eps);
+  const float f = __double2float_ru(p);
+  int32_t k = key_of(__float_as_uint(f));
+  if ((double)f == p && __fma_rn(a, eps, -p) > 0.0) k += 1;  // p exact in f32 but below a*eps
+  return k;
+}
+__device__ __forceinline__ int64_t lo_key64(int64_t b, double eps) {
+  const double a = i64_to_f64_exact(b) - 0.5;
+  const double p = __dmul_rn(a, eps);
+  return key_of((uint64_t)__double_as_longlong(p)) + (__fma_rn(a, eps, -p) > 0.0 ? 1 : 0);
+}
+template <typename T>
+__device__ __forceinline__ typename VT<T>::I lo_key(int64_t b, double eps);
+template <>
+__device__ __forceinline__ int32_t lo_key<float>(int64_t b, double eps) { return lo_key32(b, eps); }
+template <>
+__device__ __forceinline__ int64_t lo_key<double>(int64_t b, double eps) { return lo_key64(b, eps); }
+
 // Exact bin b = floor(x/eps + 1/2) (P:114 with reading G6) and the
 // double-check of the north star: returns false (escape) for non-finite x or
 // |b| > BINMAX (G8/G9).

@@ -411,7 +411,13 @@ __global__ void __launch_bounds__(kRepairThreads, 3) k_quant_flags(RepairArgs a)
     if (kp != kLow) {
       const T xp = value_of_key<T>(kp);
       I b;
-      if (quantize_fast<T>(xp, a.inv32, a.eps, a.inv, b)) lok = (I)key_of((U)as_bits(lo_t<T>((int64_t)b, a.eps)));
+      bool reg = qtry(xp, a.inv32, a.inv, b);
+      if (!reg) {  // rare: near a half-integer, huge bins, +-Inf (exact path, out of line)
+        const int64_t r = quantize_slow<T>(xp, a.eps, a.inv);
+        reg = r != kEscape;
+        b = (I)r;
+      }
+      if (reg) lok = lo_key<T>((int64_t)b, a.eps);
     }
     uint32_t wv[G::SW];  // the ballots are warp-uniform: lane 0 stores the segment
 #pragma unroll
