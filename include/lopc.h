@@ -121,6 +121,7 @@ typedef struct {
   float ms_place;             /* compress: k_chunk_scan + k_place; decompress: k_chunk_scan */
   uint32_t launches;          /* kernels this library launched in the call */
   float pass_us[16];          /* diagnostic (lopc_set_timing(2)): k_sweep pass q ended pass_us[q] us after its start */
+  uint32_t tma;               /* 1 if k_quant_flags loaded its halo boxes with TMA (LOPC_NO_TMA=1 disables) */
 } lopc_stats;
 
 int lopc_last_stats(lopc_stats* out);

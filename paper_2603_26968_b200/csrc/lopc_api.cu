@@ -166,10 +166,14 @@ int dev_info(DevInfo*& out) {
     CK(cudaFuncSetAttribute(k_encode<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     CK(cudaFuncSetAttribute(k_decode, cudaFuncAttributeMaxDynamicSharedMemorySize, dsmem));
 #define QRA(TT, ND)                                                                                      \
-  CK(cudaFuncSetAttribute(k_quant_flags<TT, ND, int32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,     \
-                          (int)quant_flags_smem<TT, ND>()));                                               \
-  CK(cudaFuncSetAttribute(k_quant_flags<TT, ND, int64_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,     \
-                          (int)quant_flags_smem<TT, ND>()));
+  CK(cudaFuncSetAttribute(k_quant_flags<TT, ND, int32_t, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                          (int)quant_flags_smem<TT, ND, false>()));                                        \
+  CK(cudaFuncSetAttribute(k_quant_flags<TT, ND, int64_t, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                          (int)quant_flags_smem<TT, ND, false>()));                                        \
+  CK(cudaFuncSetAttribute(k_quant_flags<TT, ND, int32_t, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                          (int)quant_flags_smem<TT, ND, true>()));                                         \
+  CK(cudaFuncSetAttribute(k_quant_flags<TT, ND, int64_t, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                          (int)quant_flags_smem<TT, ND, true>()));
     QRA(float, 3) QRA(float, 2) QRA(double, 3) QRA(double, 2)
 #undef QRA
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_dev.occ_sweep2, k_sweep<2, int32_t>, kSweepThreads, 0));
@@ -286,10 +290,60 @@ RepairArgs make_repair_args(const Shape& sh, const void* x, double eps, uint8_t*
 
 bool use_i32(const Shape& sh) { return sh.n < (1ull << 31) - (1ull << 24); }
 
-// a1 + a2: k_quant_flags over the tile grid.
+// TMA tensor map of x for the halo-box loads of k_quant_flags (driver entry
+// point fetched at run time: no libcuda link dependency).  Returns false when
+// TMA does not apply (unaligned base, rows not a multiple of 16 bytes).
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiledFn g_encode_tiled = nullptr;
+bool g_encode_tried = false;
+int g_use_tma = 1;  // LOPC_NO_TMA=1 in the environment disables (tests cover both paths)
+
+bool make_halo_map(const Shape& sh, const void* x, CUtensorMap* m) {
+  if (!g_use_tma || (uintptr_t)x % 16 || (sh.d2 * sh.k) % 16) return false;
+  if (sh.d0 > (1ull << 31) || sh.d1 > (1ull << 31) || sh.d2 > (1ull << 31)) return false;
+  if (!g_encode_tried) {
+    g_encode_tried = true;
+    const char* env = getenv("LOPC_NO_TMA");
+    if (env && env[0] == '1') g_use_tma = 0;
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      g_encode_tiled = reinterpret_cast<EncodeTiledFn>(fn);
+    if (!g_use_tma) return false;
+  }
+  if (!g_encode_tiled) return false;
+  const CUtensorMapDataType dt = sh.k == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64;
+  CUresult r;
+  if (sh.ndims == 3) {
+    const cuuint64_t gd[3] = {sh.d2, sh.d1, sh.d0}, gs[2] = {sh.d2 * sh.k, sh.d1 * sh.d2 * sh.k};
+    const cuuint32_t box[3] = {sh.k == 4 ? 40u : 36u, (cuuint32_t)Geo<3>::HY, (cuuint32_t)Geo<3>::HZ}, es[3] = {1, 1, 1};
+    r = g_encode_tiled(m, dt, 3, const_cast<void*>(x), gd, gs, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                       CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  } else {
+    const cuuint64_t gd[2] = {sh.d2, sh.d1}, gs[1] = {sh.d2 * sh.k};
+    const cuuint32_t box[2] = {sh.k == 4 ? 40u : 36u, (cuuint32_t)Geo<2>::HY}, es[2] = {1, 1};
+    r = g_encode_tiled(m, dt, 2, const_cast<void*>(x), gd, gs, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                       CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  }
+  return r == CUDA_SUCCESS;
+}
+
+// a1 + a2: k_quant_flags over the tile grid (TMA halo loads when possible).
 int launch_quant_flags(const Shape& sh, const RepairArgs& ra, const CLayout& L, cudaStream_t st) {
   const dim3 tgrid((unsigned)L.ntx, (unsigned)L.nty, (unsigned)L.ntz);
-#define QR(TT, ND, IX) k_quant_flags<TT, ND, IX><<<tgrid, kRepairThreads, quant_flags_smem<TT, ND>(), st>>>(ra)
+  CUtensorMap tm;
+  memset(&tm, 0, sizeof(tm));
+  const bool tma = make_halo_map(sh, ra.x, &tm);
+#define QR(TT, ND, IX)                                                                                          \
+  do {                                                                                                          \
+    if (tma)                                                                                                    \
+      k_quant_flags<TT, ND, IX, true><<<tgrid, kRepairThreads, quant_flags_smem<TT, ND, true>(), st>>>(ra, tm);   \
+    else                                                                                                        \
+      k_quant_flags<TT, ND, IX, false><<<tgrid, kRepairThreads, quant_flags_smem<TT, ND, false>(), st>>>(ra, tm); \
+  } while (0)
   if (use_i32(sh)) {
     if (sh.dtype == LOPC_F32) {
       if (sh.ndims == 3) QR(float, 3, int32_t); else QR(float, 2, int32_t);
@@ -305,6 +359,7 @@ int launch_quant_flags(const Shape& sh, const RepairArgs& ra, const CLayout& L, 
   }
 #undef QR
   CK(cudaGetLastError());
+  g_stats.tma = tma ? 1 : 0;
   return LOPC_OK;
 }
 

@@ -37,6 +37,7 @@
 // scheduling.
 #pragma once
 #include <cooperative_groups.h>
+#include <cuda.h>  // CUtensorMap (TMA halo loads)
 
 #include <type_traits>
 
@@ -351,25 +352,43 @@ __device__ __forceinline__ bool tile_interior(Idx z0, Idx y0, Idx x0, Idx d0, Id
 // lo key = max, so it has no incoming arcs, O8).  Halo points therefore need
 // only their key; only the tile's own points are quantized.
 // ---------------------------------------------------------------------------
-template <typename T, int NDIM>
-constexpr size_t quant_flags_smem() {
-  using G = Geo<NDIM>;
-  return (size_t)G::HZ * G::HY * G::HX * sizeof(typename VT<T>::I) + 16;
+// Halo box layout in shared memory.  Plain load: row stride HX (34), column
+// 0 = x0 - 1.  TMA load: the box must start on a 16-byte boundary in x (and
+// its inner extent be a multiple of 16 B), so it starts at x0 - 16/k:
+// column XO = 16/k - 1 holds x0 - 1, stride 40 (f32) / 36 (f64).
+template <typename T, int NDIM, bool TMA>
+__host__ __device__ constexpr int halo_stride() {
+  return TMA ? (sizeof(T) == 4 ? 40 : 36) : Geo<NDIM>::HX;
+}
+template <typename T, bool TMA>
+__host__ __device__ constexpr int halo_xoff() {
+  return TMA ? 16 / (int)sizeof(T) - 1 : 0;
 }
 
-template <typename T, int NDIM, typename Idx>
-__global__ void __launch_bounds__(kRepairThreads, 3) k_quant_flags(RepairArgs a) {
+template <typename T, int NDIM, bool TMA = false>
+constexpr size_t quant_flags_smem() {
+  using G = Geo<NDIM>;
+  return (size_t)G::HZ * G::HY * halo_stride<T, NDIM, TMA>() * sizeof(typename VT<T>::I) + 128;
+}
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+template <typename T, int NDIM, typename Idx, bool TMA>
+__global__ void __launch_bounds__(kRepairThreads, 3) k_quant_flags(RepairArgs a, const __grid_constant__ CUtensorMap tmap) {
   using G = Geo<NDIM>;
   using I = typename VT<T>::I;
   using U = typename VT<T>::U;
   using HR = HaloRows<NDIM>;
+  constexpr int HXS = halo_stride<T, NDIM, TMA>();
+  constexpr int XO = halo_xoff<T, TMA>();
   constexpr int TP = G::TZ * G::TY * G::TX;
   constexpr int PPT = TP / kRepairThreads;
   constexpr int D = G::D;
+  constexpr int NB = G::HZ * G::HY * HXS;  // halo box elements
   constexpr I kLow = (I)VT<T>::kSentinel;                                    // NaN / outside the grid
   constexpr I kHigh = (I)(((typename std::make_unsigned<I>::type)kLow) - 1u);  // max: escaped p
 
-  extern __shared__ __align__(16) uint8_t qf_smem[];
+  extern __shared__ __align__(128) uint8_t qf_smem[];
   I* K = reinterpret_cast<I*>(qf_smem);
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -378,8 +397,55 @@ __global__ void __launch_bounds__(kRepairThreads, 3) k_quant_flags(RepairArgs a)
   const Idx z0 = (Idx)tz * G::TZ, y0 = (Idx)ty * G::TY, x0 = (Idx)tx * G::TX;
   const bool interior = tile_interior<NDIM, Idx>(z0, y0, x0, d0, d1, d2);
 
-  // halo: keys only
-  {
+  // TMA needs non-negative box coordinates: the first tile row / column /
+  // plane (halo start at -1) takes the plain load.
+  bool via_tma = false;
+  if constexpr (TMA) via_tma = x0 >= 16 / (int)sizeof(T) && y0 >= 1 && z0 >= G::ZH;
+  if (via_tma) {
+    // halo box (z0-ZH.., y0-1.., x0-1..) by one TMA tile load; out-of-grid
+    // elements arrive as 0 and are marked below
+    uint64_t* bar = reinterpret_cast<uint64_t*>(qf_smem + (size_t)NB * sizeof(U));
+    const uint32_t sb = smem_u32(bar);
+    if (tid == 0) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sb) : "memory");
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sb), "r"((uint32_t)(NB * sizeof(U)))
+                   : "memory");
+      const int cx = (int)x0 - 1 - XO, cy = (int)y0 - 1, cz = (int)z0 - G::ZH;
+      if constexpr (NDIM == 3)
+        asm volatile(
+            "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
+                smem_u32(qf_smem)),
+            "l"(reinterpret_cast<uint64_t>(&tmap)), "r"(cx), "r"(cy), "r"(cz), "r"(sb)
+            : "memory");
+      else
+        asm volatile(
+            "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+                smem_u32(qf_smem)),
+            "l"(reinterpret_cast<uint64_t>(&tmap)), "r"(cx), "r"(cy), "r"(sb)
+            : "memory");
+    }
+    __syncthreads();  // the barrier is initialised before anyone waits on it
+    uint32_t done = 0;
+    while (!done)
+      asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0; selp.u32 %0, 1, 0, p; }"
+                   : "=r"(done)
+                   : "r"(sb)
+                   : "memory");
+    const U* raw = reinterpret_cast<const U*>(qf_smem);
+    for (int i = tid; i < NB; i += kRepairThreads) {
+      const U u = raw[i];
+      bool ok = (u & ~VT<T>::kSignBit) <= VT<T>::kInfBits;  // not NaN
+      if (!interior) {
+        const int hz = i / (G::HY * HXS), hy = (i / HXS) % G::HY, hx = i % HXS;
+        const Idx gz = z0 + hz - G::ZH, gy = y0 + hy - 1, gx = x0 + hx - 1 - XO;
+        ok = ok && gz >= 0 && gz < d0 && gy >= 0 && gy < d1 && gx >= 0 && gx < d2;
+      }
+      K[i] = ok ? (I)key_of(u) : kLow;
+    }
+  } else {
+    // halo: keys only
     HaloLoad<NDIM, U, Idx> L;
     L.load(static_cast<const U*>(a.x), z0, y0, x0, d0, d1, d2, interior, (U)0);
 #pragma unroll
@@ -391,7 +457,7 @@ __global__ void __launch_bounds__(kRepairThreads, 3) k_quant_flags(RepairArgs a)
         if (r < HR::R && hx < G::HX) {
           const U u = L.v[i][e];
           const bool nan = (u & ~VT<T>::kSignBit) > VT<T>::kInfBits;
-          K[r * G::HX + hx] = (L.ok[i][e] && !nan) ? (I)key_of(u) : kLow;
+          K[r * HXS + hx + XO] = (L.ok[i][e] && !nan) ? (I)key_of(u) : kLow;
         }
       }
     }
@@ -399,13 +465,12 @@ __global__ void __launch_bounds__(kRepairThreads, 3) k_quant_flags(RepairArgs a)
   __syncthreads();
 
   // a1 + a2 (Alg. 1 loop 2): warp w, step k handles tile row (w + 16k): lane = x.
-  // Flags leave as one ballot per slot (bit plane), written by lane j as word
-  // j of the row's 32-point segment.
+  // Flags leave as one ballot per slot (bit plane); lane 0 stores the segment.
 #pragma unroll
   for (int k = 0; k < PPT; ++k) {
     const int row = warp + k * (kRepairThreads / 32);
     const int lz = row / G::TY, ly = row % G::TY;
-    const int h = ((lz + G::ZH) * G::HY + (ly + 1)) * G::HX + (lane + 1);
+    const int h = ((lz + G::ZH) * G::HY + (ly + 1)) * HXS + (lane + 1 + XO);
     const I kp = K[h];
     I lok = kHigh;
     if (kp != kLow) {
@@ -424,7 +489,7 @@ __global__ void __launch_bounds__(kRepairThreads, 3) k_quant_flags(RepairArgs a)
     for (int j = 0; j < G::SW; ++j) wv[j] = 0;
 #pragma unroll
     for (int j = 0; j < 2 * D; ++j) {
-      const I kn = K[h + slot_hoff<NDIM>(j)];
+      const I kn = K[h + slot_dz<NDIM>(j) * G::HY * HXS + slot_dy<NDIM>(j) * HXS + slot_dx<NDIM>(j)];
       const bool arc = kn >= lok && (j < D ? kn < kp : kn <= kp);
       wv[j] = __ballot_sync(0xffffffffu, arc);
     }

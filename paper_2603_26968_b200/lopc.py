@@ -37,7 +37,8 @@ class Stats(C.Structure):
         ("max_subbin", C.c_uint32), ("timing_valid", C.c_uint32)] + [
         (n, C.c_float) for n in ("ms_h2d", "ms_quant_repair", "ms_sweep", "ms_encode", "ms_decode", "ms_d2h",
                                  "ms_total")] + [("raised", C.c_uint64), ("pass_items", C.c_uint32 * 16), ("phase_cycles", C.c_uint64 * 16),
-        ("ms_place", C.c_float), ("launches", C.c_uint32), ("pass_us", C.c_float * 16)]
+        ("ms_place", C.c_float), ("launches", C.c_uint32), ("pass_us", C.c_float * 16),
+        ("tma", C.c_uint32)]
 
 
 _lib = None
