@@ -1197,7 +1197,16 @@ __device__ __forceinline__ bool h32_err(const DecodeArgs& a) {
   return (*(volatile uint32_t*)&a.ctr->err) & (kErrCorrupt | kErrVersion | kErrNoSpace);
 }
 
-// Persistent: each 2-CTA cluster takes chunk tickets until the stream is done.
+// Persistent: 2-CTA cluster k decodes chunks k, k + clusters, ... (static
+// round-robin: no ticket, so no cluster barrier at the top of the loop).
+// Per chunk: [decode own stream] -> cluster barrier (release/acquire: the
+// partner's words are complete) -> copy the partner's half -> relaxed
+// cluster barrier (both copies done; only execution order is needed, so the
+// outstanding output stores are not waited for) -> reconstruct from local smem.
+__device__ __forceinline__ void cluster_sync_relaxed() {
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;\n\tbarrier.cluster.wait.aligned;" ::: "memory");
+}
+
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kCodecThreads, 4) k_decode(DecodeArgs a) {
   namespace cg = cooperative_groups;
   extern __shared__ __align__(16) uint8_t smem_raw[];
@@ -1206,7 +1215,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kCodecThreads, 4) k_
   const int tid = threadIdx.x;
   const int r = (int)cl.block_rank();
   // every exit below is taken by both CTAs of the cluster (same header, same
-  // flag word, same ticket) so the cluster barriers stay matched
+  // flag word, same chunk sequence) so the cluster barriers stay matched
   const Hdr h = parse_header(a);
   if (!h.ok) {
     if (blockIdx.x == 0 && tid == 0) atomicOr(&a.ctr->err, h.err);
@@ -1215,26 +1224,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kCodecThreads, 4) k_
   if (h32_err(a)) return;  // k_chunk_scan flagged the table
   const uint64_t ncnk = a.slab ? a.c_count : (uint64_t)h.C;
   const DecSmem* s0 = cl.map_shared_rank(&sm, 0);
-  DecSmem* s1 = cl.map_shared_rank(&sm, 1);
+  const DecSmem* s1 = cl.map_shared_rank(&sm, 1);
   if (tid == 0) sm.bad = 0;  // sticky: a corrupt chunk fails the whole call
-  for (;;) {
-    if (tid == 0) {
-      if (r == 0) {  // rank 0 draws the ticket and pushes it into both CTAs
-        const uint32_t t = atomicAdd(&a.ctr->ticket, 1u);
-        sm.ticket = t;
-        s1->ticket = t;
-      }
-    }
-    cl.sync();  // ticket visible; the partner finished reading our words
-    const uint32_t l = sm.ticket;  // local copy: the partner may exit after this barrier
-    if (l >= ncnk) break;
+  cl.sync();                 // both flags initialised
+  const uint64_t nclu = gridDim.x / 2;
+  for (uint64_t l = blockIdx.x / 2; l < ncnk; l += nclu) {
+    __syncthreads();  // this CTA's previous reconstruct is done with its smem
     const uint32_t sz = a.table[2 * l + r];
     const uint8_t* p = a.base + a.off[l] + (r ? a.table[2 * l] : 0u);
     if (h.dtype == 0)
       decode_stream<float>(a, p, sz, r != 0, sm);
     else
       decode_stream<double>(a, p, sz, r != 0, sm);
-    cl.sync();
+    cl.sync();  // release/acquire: the partner's words are complete
     const uint64_t c = a.c_begin + l;
     const bool ok = !s0->bad && !s1->bad;
     // the partner's words of this CTA's half, copied once into local smem
@@ -1245,18 +1247,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kCodecThreads, 4) k_
       uint4* loc = reinterpret_cast<uint4*>(sm.O);
       for (int t = tid; t < HB / 16; t += kCodecThreads) loc[t] = rem[t];
     }
-    cl.sync();  // remote reads done (the partner may overwrite its words next); local copy visible
+    cluster_sync_relaxed();  // both copies done: the partner may overwrite its words next
+    __syncthreads();         // the local copy is visible to the whole CTA
     if (ok) {
       const int half_w = h.dtype == 0 ? 2048 : 1024;  // W / 2
       const uint8_t* own = sm.Wd;
       if (h.dtype == 0)
-        reconstruct_half<float>(a, h, (uint32_t)c, r, r ? sm.O : own, r ? half_w : 0, r ? own : sm.O,
-                                r ? 0 : half_w * 0);
+        reconstruct_half<float>(a, h, (uint32_t)c, r, r ? sm.O : own, r ? half_w : 0, r ? own : sm.O, 0);
       else
-        reconstruct_half<double>(a, h, (uint32_t)c, r, r ? sm.O : own, r ? half_w : 0, r ? own : sm.O,
-                                 r ? 0 : half_w * 0);
+        reconstruct_half<double>(a, h, (uint32_t)c, r, r ? sm.O : own, r ? half_w : 0, r ? own : sm.O, 0);
     }
   }
+  cl.sync();  // no CTA leaves while its partner may still read its flags
 }
 
 }  // namespace lopc
