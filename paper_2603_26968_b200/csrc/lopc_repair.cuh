@@ -868,12 +868,8 @@ __global__ void __launch_bounds__(kSweepThreads, 3) k_sweep(RepairArgs a) {
 template <int NDIM, typename Idx>
 __global__ void __launch_bounds__(256) k_ghost_inject(RepairArgs a, const uint32_t* __restrict__ recv, int64_t g0,
                                                       int64_t count) {
-  using G = Geo<NDIM>;
-  constexpr int D = G::D;
-  constexpr int SW = G::SW;
   const int lane = threadIdx.x & 31;
-  const Idx d0 = (Idx)a.d0, d1 = (Idx)a.d1, d2 = (Idx)a.d2, plane = d1 * d2;
-  const size_t nseg = (size_t)a.nseg;
+  const Idx d1 = (Idx)a.d1, d2 = (Idx)a.d2, plane = d1 * d2;
   unsigned changed = 0;
   const int64_t wstep = (int64_t)gridDim.x * blockDim.x;
   for (int64_t ib = (int64_t)(blockIdx.x * blockDim.x + (threadIdx.x & ~31)); ib < count; ib += wstep) {
