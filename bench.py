@@ -175,8 +175,9 @@ def run_reference(args, rank, world):
         if i >= args.warmup:
             times.append(v)
     value = statistics.median(times)
+    nbytes = x[: max(1, x.shape[0] // 12) if x.ndim == 3 else max(1, x.shape[0] // 8)].nbytes
     line = {"metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": args.gpus, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": nbytes / (value * 1e9) * 1e3, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic", "impl": "reference",
             "config": {"workload": WORKLOAD[args.config], "sample": "bounded crop, see cpu_baseline"},
             "cpu_baseline": {"value": value, "unit": "GB/s", "cores": 1, "kind": "oracle", "sample": desc},

@@ -83,8 +83,10 @@ prof = os.path.join(ROOT, "profiles")
 os.makedirs(prof, exist_ok=True)
 json.dump({"source": f"ncu --set full --clock-control none, tools/prof_step.py {config} (second step)",
            "kernels": out}, open(os.path.join(prof, f"{tag}_ncu_summary.json"), "w"), indent=1)
-traffic = {f"k_{k}" if not k.startswith("k_") else k: (v["dram_read_bytes"] or 0) + (v["dram_write_bytes"] or 0)
-           for k, v in out.items()}
+traffic = {}
+for k, v in out.items():
+    name = k[:-2] if k.endswith("_2") and k.startswith("k_encode") else k  # the two encode roles: one step's encode
+    traffic[name] = traffic.get(name, 0) + (v["dram_read_bytes"] or 0) + (v["dram_write_bytes"] or 0)
 json.dump(traffic, open(os.path.join(prof, f"traffic_{config}.json"), "w"), indent=1)
 
 # launch list: our kernels only, plus each kernel's share of the step
