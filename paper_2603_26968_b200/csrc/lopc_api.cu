@@ -649,6 +649,8 @@ int lopc_compress_ex(const void* in, int ndims, const uint64_t* dims, int dtype,
   for (int i = 0; i < 16; ++i) g_stats.pass_items[i] = hc->pass_items[i];
   for (int i = 0; i < 16; ++i) g_stats.phase_cycles[i] = hc->phase[i];
   for (int i = 0; i < 16; ++i) g_stats.pass_us[i] = (float)(hc->pass_ns[i] * 1e-3);
+  if (g_timing >= 2)  // diagnostic: dense-pass cycles per phase (levels, s write, border) in phase_cycles[5..7]
+    for (int i = 1; i < 4; ++i) g_stats.phase_cycles[4 + i] += hc->dense_cycles[i];
   uint32_t err = hc->err;
   if (hc->passes >= (unsigned long long)(1 << 20) && hc->list_count[(hc->passes + 1) % 3] != 0) err |= kErrPassCap;
   if ((rc = map_err(err & ~kErrNoSpace))) return rc;

@@ -121,6 +121,7 @@ struct Counters {
   unsigned long long phase[16];      // diagnostic: SM cycles per codec phase (lopc_set_timing(2))
   unsigned long long ghost_changed;  // slab mode: ghosts raised by the last k_ghost_inject
   unsigned long long pass_ns[kPassHist];  // diagnostic (prof): k_sweep pass end times, ns after the launch
+  unsigned long long dense_cycles[4];     // diagnostic (prof): dense pass load / levels / s write / border, per warp
 };
 
 // Diagnostic phase clock: thread 0 of a block adds the cycles since the last
@@ -613,6 +614,7 @@ __global__ void __launch_bounds__(kSweepThreads, 3) k_sweep(RepairArgs a) {
           if (4 * q + t < 2 * D) F[i][4 * q + t] = ws[t];
       }
     }
+    long long tc0 = a.prof ? clock64() : 0;
     uint32_t cnt[2][kLevelPlanes];
 #pragma unroll
     for (int i = 0; i < 2; ++i)
@@ -681,6 +683,7 @@ __global__ void __launch_bounds__(kSweepThreads, 3) k_sweep(RepairArgs a) {
       __syncwarp();
       if (L == kMaxLevel) break;  // hand the rest to the worklist
     }
+    long long tc1 = a.prof ? clock64() : 0;
     const bool capped = L == kMaxLevel;
     const int top = capped ? kMaxLevel : L - 1;  // highest non-empty level
     const int nplanes = 32 - __clz(top | 1);
@@ -701,6 +704,7 @@ __global__ void __launch_bounds__(kSweepThreads, 3) k_sweep(RepairArgs a) {
       const Idx gz = z0 + rz, gy = y0 + ry, gx = x0 + lane;
       if (gz < d0 && gy < d1 && gx < d2) __stcg(&a.s[(gz * d1 + gy) * d2 + gx], sv);
     }
+    long long tc2 = a.prof ? clock64() : 0;
     // border points with s > 0 feed out-of-tile points that assumed s = 0
     // (all lanes stay converged: the enqueues are warp-collective)
 #pragma unroll
@@ -716,29 +720,83 @@ __global__ void __launch_bounds__(kSweepThreads, 3) k_sweep(RepairArgs a) {
         }
       }
       if (!__any_sync(0xffffffffu, lv != 0)) continue;
-#pragma unroll 1
+      // all neighbour flag words first (independent loads, one latency), then
+      // the feeds and their enqueues
+      uint32_t win[2 * D], wed[2 * D];
+#pragma unroll
       for (int j = 0; j < 2 * D; ++j) {
         const int dz = slot_dz<NDIM>(j), dy = slot_dy<NDIM>(j), dx = slot_dx<NDIM>(j);
         const int tlz = lz[i] + dz, tly = ly[i] + dy;
         const bool row_in = tlz >= 0 && tlz < G::TZ && tly >= 0 && tly < G::TY;
-        uint32_t cand = row_in ? (lv & (dx > 0 ? 0x80000000u : (dx < 0 ? 1u : 0u))) : lv;
         const Idx gz = z0 + tlz, gy = y0 + tly;
-        if (gz < 0 || gz >= d0 || gy < 0 || gy >= d1) cand = 0;
-        uint32_t feed = 0;
-        if (cand) {
-          const int jo = slot_opp<NDIM>(j);
-          const uint32_t* rowf = a.flags + ((size_t)(gz * d1 + gy) * nseg) * SW + jo;
-          const uint32_t inseg = cand & (dx > 0 ? 0x7fffffffu : (dx < 0 ? 0xfffffffeu : 0xffffffffu));
-          if (inseg) feed |= inseg & xshift(__ldg(rowf + (size_t)tx * SW), dx);
-          if (dx > 0 && (cand >> 31) && x0 + 32 < d2 && (__ldg(rowf + (size_t)(tx + 1) * SW) & 1u)) feed |= 0x80000000u;
-          if (dx < 0 && (cand & 1u) && tx > 0 && (__ldg(rowf + (size_t)(tx - 1) * SW) >> 31)) feed |= 1u;
+        const bool gin = gz >= 0 && gz < d0 && gy >= 0 && gy < d1;
+        const uint32_t cand = !gin ? 0u : (row_in ? (lv & (dx > 0 ? 0x80000000u : (dx < 0 ? 1u : 0u))) : lv);
+        const uint32_t* rowf = a.flags + ((size_t)(gin ? gz * d1 + gy : 0) * nseg) * SW + slot_opp<NDIM>(j);
+        const uint32_t inseg = cand & (dx > 0 ? 0x7fffffffu : (dx < 0 ? 0xfffffffeu : 0xffffffffu));
+        win[j] = inseg ? __ldg(rowf + (size_t)tx * SW) : 0u;
+        wed[j] = 0;
+        if (dx > 0 && (cand >> 31) && x0 + 32 < d2) wed[j] = __ldg(rowf + (size_t)(tx + 1) * SW);
+        if (dx < 0 && (cand & 1u) && tx > 0) wed[j] = __ldg(rowf + (size_t)(tx - 1) * SW);
+      }
+      // feeds of all slots; each slot's candidates are consecutive points of
+      // one row, so their dedup bits lie in <= 2 bitmap words: <= 2 atomics
+      // per slot, all issued before any result is used, then one list
+      // reservation for the whole warp
+      uint32_t fresh[2 * D];
+      Idx fbase[2 * D];
+#pragma unroll
+      for (int j = 0; j < 2 * D; ++j) {
+        const int dz = slot_dz<NDIM>(j), dy = slot_dy<NDIM>(j), dx = slot_dx<NDIM>(j);
+        const int tlz = lz[i] + dz, tly = ly[i] + dy;
+        const bool row_in = tlz >= 0 && tlz < G::TZ && tly >= 0 && tly < G::TY;
+        const Idx gz = z0 + tlz, gy = y0 + tly;
+        const bool gin = gz >= 0 && gz < d0 && gy >= 0 && gy < d1;
+        const uint32_t cand = !gin ? 0u : (row_in ? (lv & (dx > 0 ? 0x80000000u : (dx < 0 ? 1u : 0u))) : lv);
+        const uint32_t inseg = cand & (dx > 0 ? 0x7fffffffu : (dx < 0 ? 0xfffffffeu : 0xffffffffu));
+        uint32_t feed = inseg & xshift(win[j], dx);
+        if (dx > 0 && (cand >> 31) && (wed[j] & 1u)) feed |= 0x80000000u;
+        if (dx < 0 && (cand & 1u) && (wed[j] >> 31)) feed |= 1u;
+        Idx base = gin ? (gz * d1 + gy) * d2 + x0 + dx : 0;  // point of feed bit 0
+        if (base < 0) {  // only row 0, x0 = 0, dx = -1: feed bit 0 is clear there
+          feed >>= 1;
+          base += 1;
         }
-        while (__any_sync(0xffffffffu, feed != 0)) {
-          const int x = feed ? __ffs(feed) - 1 : 0;
-          enqueue_warp<Idx>(a, (gz * d1 + gy) * d2 + x0 + x + dx, feed != 0, 2);
-          feed &= feed - 1;
+        fbase[j] = base;
+        fresh[j] = feed;
+        if (feed) {
+          const uint32_t sh = (uint32_t)base & 31u;
+          uint32_t* bw = a.bitmap + ((UIdx)base >> 5);
+          const uint32_t m0 = feed << sh, m1 = sh ? feed >> (32u - sh) : 0u;
+          const uint32_t o0 = m0 ? atomicOr(bw, m0) : 0u;
+          const uint32_t o1 = m1 ? atomicOr(bw + 1, m1) : 0u;
+          fresh[j] = ((~o0 & m0) >> sh) | (sh ? ((~o1 & m1) << (32u - sh)) : 0u);
         }
       }
+      uint32_t c = 0;
+#pragma unroll
+      for (int j = 0; j < 2 * D; ++j) c += __popc(fresh[j]);
+      uint32_t incl = c;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+      }
+      const uint32_t wtot = __shfl_sync(0xffffffffu, incl, 31);
+      if (wtot) {
+        unsigned long long pos = 0;
+        if (lane == 31) pos = atomicAdd(&a.ctr->list_count[2], (unsigned long long)wtot);
+        pos = __shfl_sync(0xffffffffu, pos, 31) + (incl - c);
+        UIdx* Lst = static_cast<UIdx*>(a.plist);  // pass 2 list: (2 & 1) * cap = 0
+#pragma unroll
+        for (int j = 0; j < 2 * D; ++j)
+          for (uint32_t m = fresh[j]; m; m &= m - 1) Lst[pos++] = (UIdx)(fbase[j] + (__ffs(m) - 1));
+      }
+    }
+    if (a.prof && lane == 0) {
+      const long long tc3 = clock64();
+      atomicAdd(&a.ctr->dense_cycles[1], (unsigned long long)(tc1 - tc0));
+      atomicAdd(&a.ctr->dense_cycles[2], (unsigned long long)(tc2 - tc1));
+      atomicAdd(&a.ctr->dense_cycles[3], (unsigned long long)(tc3 - tc2));
     }
     if (lane == 0) tile = atomicAdd(&a.ctr->tile_ticket, 1u);
     tile = __shfl_sync(0xffffffffu, tile, 0);

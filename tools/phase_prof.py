@@ -27,6 +27,8 @@ for i, n in enumerate(enc):
     print(f"  enc {n:22s} {sc['phase_cycles'][i] / C:10.0f}")
 for i, n in dec.items():
     print(f"  dec {n:22s} {sd['phase_cycles'][i] / C:10.0f}")
+print("  dense pass cycles per tile: levels %.0f, s write %.0f, border %.0f" % tuple(
+    (sc["phase_cycles"][4 + i] - 0) / max(1, sc["n_tiles"]) for i in (1, 2, 3)))
 print("  sweep pass end times (us):", [round(v, 1) for v in sc["pass_us"] if v], "items", sc["pass_items"][:10])
 print(f"  sweep dense pass {sc['phase_cycles'][14] / 1e3:.1f} us, sparse passes {sc['phase_cycles'][15] / 1e3:.1f} us")
 print({k: (sc[k], sd[k]) for k in ("ms_quant_repair", "ms_sweep", "ms_encode", "ms_place", "ms_decode")})
