@@ -10,10 +10,11 @@ steps by writing a 512 MB buffer outside the timed events.
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg2]
   python bench.py --impl reference ...   # the CPU oracle arm (rank 0 only)
 
-Multi-GPU (torchrun): every rank compresses its own field of the chosen
-config (weak scaling, no data-path collective: the slab mode with halo
-exchange is not built yet); the barrier + max-over-ranks
-timing of the contract is kept.
+Multi-GPU (torchrun): the slab mode — one global field, the
+config tiled N times along z (cfg1-4) or the cfg5 turbulence field with 256 z
+planes of 2048^2 f64 per rank (N = 8 is cfg5 itself), NCCL halo exchange per
+repair round; weak scaling, barrier + max-over-ranks device time.
+`--config cfg5` at N = 1 runs one rank's slab (2048 x 2048 x 256 f64).
 """
 from __future__ import annotations
 
@@ -39,7 +40,10 @@ WORKLOAD = {
     "cfg2": "cfg2: 3D f32 100x500x500 Isabel-shaped synthetic field, NOA 1e-3",
     "cfg3": "cfg3: 3D f32 512^3 NYX-shaped log-normal density, NOA 1e-4",
     "cfg4": "cfg4: 2D f32 1800x3600 CESM-ATM-shaped field with near-ties, NOA 1e-3",
+    "cfg5": "cfg5: 3D f64 turbulence (Kolmogorov mode sum), 2048x2048 planes, 256 z-planes per GPU "
+            "(N=8: the 2048^3 field), NOA 1e-5 of the global range",
 }
+CFG5_PLANES = 256  # z-planes of 2048^2 per rank
 
 
 def load_peaks():
@@ -113,6 +117,13 @@ def cpu_model():
     return "unknown"
 
 
+def crop_planes(x) -> int:
+    """Leading z-planes (3D) / rows (2D) of the bounded oracle sample: about
+    2-8 M points, a few seconds of single-thread oracle work."""
+    per = int(np.prod(x.shape[1:]))
+    return max(1, min(x.shape[0] // 12 if x.ndim == 3 else x.shape[0] // 8, (2 << 20) // per))
+
+
 def oracle_sample(cfg_name: str, x: np.ndarray, eps: float, budget_s: float):
     """The CPU oracle (single thread) on a bounded crop of the same field:
     leading z-planes (3D) or rows (2D), compress + decompress, repeated until
@@ -120,7 +131,7 @@ def oracle_sample(cfg_name: str, x: np.ndarray, eps: float, budget_s: float):
     import oracle
 
     oracle.build()
-    planes = max(1, x.shape[0] // 12) if x.ndim == 3 else max(1, x.shape[0] // 8)
+    planes = crop_planes(x)
     crop = np.ascontiguousarray(x[:planes])
     t0 = time.perf_counter()
     done = 0
@@ -144,7 +155,7 @@ def omp_sample(cfg_name: str, x: np.ndarray, eps: float, budget_s: float):
     the same bounded crop, compress only (GB/s of raw input)."""
     import oracle
 
-    planes = max(1, x.shape[0] // 12) if x.ndim == 3 else max(1, x.shape[0] // 8)
+    planes = crop_planes(x)
     crop = np.ascontiguousarray(x[:planes])
     st, _ = oracle.omp_compress(crop, eps)  # warm-up (thread pool, build)
     t0 = time.perf_counter()
@@ -161,12 +172,33 @@ def omp_sample(cfg_name: str, x: np.ndarray, eps: float, budget_s: float):
                       f"({crop.nbytes / 1e6:.1f} MB) x{reps}, {sweeps} relaxation sweeps, {cpu_model()}"}
 
 
+def cfg5_eps(world: int) -> float:
+    """a0 for the cfg5 weak-scaling field (256 planes per rank): 1e-5 x its
+    range, found block by block on the device (same value on every rank)."""
+    from synth import turbulence as turb
+
+    lo, hi = turb.field_range(CFG5_PLANES * world, 2048, 2048)
+    return turb.eps_noa_range(lo, hi, turb.CFG5_REL)
+
+
 def run_reference(args, rank, world):
     if rank != 0:
         return
-    cfg = CONFIGS[args.config]
-    x = cfg.generate()
-    eps = eps_noa(x, cfg.rel)
+    if args.config == "cfg5":
+        # the oracle's sample: the leading planes of the same field, built on
+        # the host (the crop is all the reference arm touches); eps of the
+        # N-rank field, as the lopc arm uses
+        from synth import turbulence as turb
+
+        x = turb.planes_torch(0, 1, 2048, 2048, device="cpu").numpy()
+        try:
+            eps = cfg5_eps(world)
+        except Exception:  # no GPU on this host: the range of the crop
+            eps = eps_noa(x, turb.CFG5_REL)
+    else:
+        cfg = CONFIGS[args.config]
+        x = cfg.generate()
+        eps = eps_noa(x, cfg.rel)
     times = []
     desc = ""
     per = max(2.0, 60.0 / max(1, args.steps + args.warmup))
@@ -175,10 +207,11 @@ def run_reference(args, rank, world):
         if i >= args.warmup:
             times.append(v)
     value = statistics.median(times)
-    nbytes = x[: max(1, x.shape[0] // 12) if x.ndim == 3 else max(1, x.shape[0] // 8)].nbytes
+    nbytes = x[:crop_planes(x)].nbytes
     line = {"metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": nbytes / (value * 1e9) * 1e3, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f32", "data": "synthetic", "impl": "reference",
+            "vs_baseline": None, "dtype": "f32" if x.dtype == np.float32 else "f64", "data": "synthetic",
+            "impl": "reference",
             "config": {"workload": WORKLOAD[args.config], "sample": "bounded crop, see cpu_baseline"},
             "cpu_baseline": {"value": value, "unit": "GB/s", "cores": 1, "kind": "oracle", "sample": desc},
             "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -228,13 +261,29 @@ def run_slabs(args, rank, world, local):
     uid = [lopc.comm_unique_id() if rank == 0 else None]
     dist.broadcast_object_list(uid, src=0)
     comm = lopc.Comm(world, rank, uid[0])
-    base, eps, shape = tiled_config(args.config, world)
-    dt = torch.float32 if base.dtype == np.float32 else torch.float64
-    b = lopc.slab_partition(shape, dt, world)
-    e0, e1 = b[rank], b[rank + 1]
-    xs_np = slab_values(base, shape, e0, e1)
-    xs = torch.from_numpy(xs_np).cuda()
-    k = xs_np.itemsize
+    if args.config == "cfg5":
+        from synth import turbulence as turb
+
+        shape = (CFG5_PLANES * world, 2048, 2048)
+        dt = torch.float64
+        b = lopc.slab_partition(shape, dt, world)
+        e0, e1 = b[rank], b[rank + 1]
+        P = shape[1] * shape[2]
+        assert e0 % P == 0 and e1 % P == 0
+        xs = turb.planes_torch(e0 // P, e1 // P, shape[1], shape[2]).reshape(-1)
+        mm = torch.stack([-xs.min(), xs.max()])
+        dist.all_reduce(mm, op=dist.ReduceOp.MAX)  # a0: the global range
+        eps = turb.eps_noa_range(-float(mm[0]), float(mm[1]), turb.CFG5_REL)
+        xs_np = None
+        k = 8
+    else:
+        base, eps, shape = tiled_config(args.config, world)
+        dt = torch.float32 if base.dtype == np.float32 else torch.float64
+        b = lopc.slab_partition(shape, dt, world)
+        e0, e1 = b[rank], b[rank + 1]
+        xs_np = slab_values(base, shape, e0, e1)
+        xs = torch.from_numpy(xs_np).cuda()
+        k = xs_np.itemsize
     W = 16384 // k
     n_chunks = -(-int(np.prod(shape)) // W)
     out = torch.empty(lopc.slab_bound(shape, dt, e0, e1), dtype=torch.uint8, device="cuda")
@@ -252,10 +301,16 @@ def run_slabs(args, rank, world, local):
     for _ in range(args.warmup):
         loc, po, tot = step()
     torch.cuda.synchronize()
-    import oracle  # test infrastructure, outside the timed region: per-rank bound check
+    if xs_np is not None:
+        import oracle  # test infrastructure, outside the timed region: per-rank bound check
 
-    y_np = y.cpu().numpy().reshape(1, -1)
-    bound_bad = oracle.bound_violations(xs_np.reshape(1, -1), y_np, eps)
+        y_np = y.cpu().numpy().reshape(1, -1)
+        bound_bad = oracle.bound_violations(xs_np.reshape(1, -1), y_np, eps)
+        order_bad = None
+    else:  # cfg5 slab (1 G points): the device checker (k_check, pinned to the oracle's checkers)
+        lsh = ((e1 - e0) // (shape[1] * shape[2]),) + tuple(shape[1:])
+        chk = lopc.check(xs.view(lsh), y.view(lsh), eps)
+        bound_bad, order_bad = chk["bound_violations"], chk["order_violations"]
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
     comp_ms, dec_ms = [], []
     dist.barrier()
@@ -275,10 +330,10 @@ def run_slabs(args, rank, world, local):
     torch.cuda.synchronize()
     lopc.compress_slab(comm, xs, shape, eps, e0, e1, out=out)
     st = lopc.last_stats()
-    t = torch.tensor([sum(comp_ms) + sum(dec_ms), sum(comp_ms), sum(dec_ms), float(bound_bad)], device="cuda",
-                     dtype=torch.float64)
+    t = torch.tensor([sum(comp_ms) + sum(dec_ms), sum(comp_ms), sum(dec_ms), float(bound_bad),
+                      float(order_bad or 0)], device="cuda", dtype=torch.float64)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    total_ms, cm, dm, bad = (float(v) for v in t.tolist())
+    total_ms, cm, dm, bad, obad = (float(v) for v in t.tolist())
     K = args.steps
     raw_total = int(np.prod(shape)) * k
     value = raw_total * K / (total_ms / 1e3) / 1e9
@@ -297,7 +352,7 @@ def run_slabs(args, rank, world, local):
         launches += sc["launches"] + sd["launches"]
     lopc.set_timing(False)
     # e2e: pinned host slab in, local stream out and back, values out
-    xh = torch.from_numpy(xs_np).pin_memory()
+    xh = torch.from_numpy(xs_np).pin_memory() if xs_np is not None else xs.cpu().pin_memory()
     oh = torch.empty(out.numel(), dtype=torch.uint8).pin_memory()
     yh = torch.empty(e1 - e0, dtype=dt).pin_memory()
     e2e = []
@@ -338,12 +393,15 @@ def run_slabs(args, rank, world, local):
             "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": K, "warmup": args.warmup,
             "ms_per_step": total_ms / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f32" if k == 4 else "f64", "data": "synthetic",
-            "config": {"workload": WORKLOAD[args.config] + f", tiled x{world} along z (mirrored), slab mode",
+            "config": {"workload": WORKLOAD[args.config] + (
+                           ", slab mode" if args.config == "cfg5" else f", tiled x{world} along z (mirrored), slab mode"),
                        "dims": list(shape), "eps": eps, "ranges": b, "l2": "flushed (512 MB write) between steps",
                        "parallelism": f"slabs x{world}: NCCL halo exchange per repair round"},
             "compress_GBps": raw_total * K / (cm / 1e3) / 1e9, "decompress_GBps": raw_total * K / (dm / 1e3) / 1e9,
             "ratio": raw_total / stream_total, "stream_bytes": stream_total, "bound_violations": int(bad),
-            "order_violations": None, "repair_rounds": st["inner_iters"],
+            "order_violations": None if xs_np is not None else int(obad),
+            "order_check": "per-rank slab, device k_check" if xs_np is None else None,
+            "repair_rounds": st["inner_iters"],
             "per_kernel_rank0": {kk: {"ms": med[kk], "alg_bytes": alg[kk]} for kk in med},
             "roofline": {"kernel": f"k_{dom}", "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src},
@@ -391,11 +449,19 @@ def main():
 
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     lopc.load()
-    cfg = CONFIGS[args.config]
-    x_np = cfg.generate()
-    eps = eps_noa(x_np, cfg.rel)
-    x = torch.from_numpy(x_np).cuda()
-    raw = x_np.nbytes
+    big = args.config == "cfg5"
+    if big:  # one rank's slab of cfg5, generated on the device (8.6 GB f64)
+        from synth import turbulence as turb
+
+        x = turb.planes_torch(0, CFG5_PLANES, 2048, 2048)
+        eps = cfg5_eps(1)
+        x_np = None
+    else:
+        cfg = CONFIGS[args.config]
+        x_np = cfg.generate()
+        eps = eps_noa(x_np, cfg.rel)
+        x = torch.from_numpy(x_np).cuda()
+    raw = x.numel() * x.element_size()
     flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
     st_buf = torch.empty(lopc.compress_bound(x.shape, x.dtype), dtype=torch.uint8, device="cuda")
     y = torch.empty_like(x)
@@ -409,11 +475,15 @@ def main():
         st = step()
     torch.cuda.synchronize()
     # correctness of the benchmarked configuration: order / bound / stability
-    import oracle  # test infrastructure, outside the timed region
+    if big:  # 1 G points: the device checker (k_check == the oracle's checkers, tests/test_gpu_check.py)
+        chk = lopc.check(x, y, eps)
+        violations, bound_bad = chk["order_violations"], chk["bound_violations"]
+    else:
+        import oracle  # test infrastructure, outside the timed region
 
-    y_np = y.cpu().numpy()
-    violations = oracle.order_violations(x_np, y_np) if rank == 0 else 0
-    bound_bad = oracle.bound_violations(x_np, y_np, eps) if rank == 0 else 0
+        y_np = y.cpu().numpy()
+        violations = oracle.order_violations(x_np, y_np) if rank == 0 else 0
+        bound_bad = oracle.bound_violations(x_np, y_np, eps) if rank == 0 else 0
     nbytes_stream = int(st.numel())
 
     # (1) the timed region: K steps, CUDA events around the C-ABI calls
@@ -473,9 +543,9 @@ def main():
     value = raw * world * K / (total_ms / 1e3) / 1e9
 
     # ---- e2e through the C-ABI with HOST (pinned) buffers -------------------
-    xh = torch.from_numpy(x_np).pin_memory()
+    xh = x.cpu().pin_memory()
     sth = torch.empty(st_buf.numel(), dtype=torch.uint8).pin_memory()
-    yh = torch.empty(x_np.shape, dtype=torch.float32 if x_np.dtype == np.float32 else torch.float64).pin_memory()
+    yh = torch.empty(x.shape, dtype=x.dtype).pin_memory()
     for _ in range(2):
         s2 = lopc.compress(xh, eps, out=sth)
         lopc.decompress(s2, out=yh)
@@ -503,9 +573,9 @@ def main():
     # algorithmic bytes per launch: x is k bytes/point, the
     # bit-plane flags F = 2 (3D) / 1 (2D) bytes/point, s is u32.
     peak, peak_src = load_peaks()
-    n = x_np.size
-    k = x_np.itemsize
-    F = 2 if x_np.ndim == 3 else 1
+    n = x.numel()
+    k = x.element_size()
+    F = 2 if x.dim() == 3 else 1
     med = {kk: statistics.median(v) for kk, v in kern.items()}
     alg = {
         "quant_flags": n * (k + F),                                        # read x, write flags
@@ -526,22 +596,25 @@ def main():
 
     cpu = cpu_omp = None
     if not args.no_cpu_baseline:
-        v, desc = oracle_sample(args.config, x_np, eps, args.cpu_budget)
+        xs_host = x_np if x_np is not None else x[:1].cpu().numpy()  # cfg5: the leading plane
+        v, desc = oracle_sample(args.config, xs_host, eps, args.cpu_budget)
         cpu = {"value": v, "unit": "GB/s", "cores": 1, "kind": "oracle", "sample": desc}
-        cpu_omp = omp_sample(args.config, x_np, eps, max(2.0, args.cpu_budget / 2))
+        cpu_omp = omp_sample(args.config, xs_host, eps, max(2.0, args.cpu_budget / 2))
 
     line = {
         "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": K, "warmup": args.warmup,
         "ms_per_step": total_ms / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f32" if k == 4 else "f64", "data": "synthetic",
-        "config": {"workload": WORKLOAD[args.config], "dims": list(x_np.shape), "eps": eps,
-                   "input_sha256": sha256(x_np), "l2": "flushed (512 MB write) between steps",
+        "config": {"workload": WORKLOAD[args.config] + (", one rank's slab at N=1" if big else ""),
+                   "dims": list(x.shape), "eps": eps,
+                   "input_sha256": sha256(x_np) if x_np is not None else "generated on the device (synth/turbulence.py)",
+                   "l2": "flushed (512 MB write) between steps" if not big else "inputs (8.6 GB) larger than L2",
                    "parallelism": f"replicas x{world}" if world > 1 else "single GPU"},
         "compress_GBps": raw * world * K / (cm / 1e3) / 1e9,
         "step_ms": {"compress": [round(v, 4) for v in comp_ms], "decompress": [round(v, 4) for v in dec_ms]},
         "decompress_GBps": raw * world * K / (dm / 1e3) / 1e9,
         "ratio": raw / nbytes_stream, "stream_bytes": nbytes_stream,
-        "order_violations": violations, "bound_violations": bound_bad,
+        "order_violations": int(violations), "bound_violations": bound_bad,
         "repair": rep,
         "per_kernel": per_kernel,
         "roofline": {"kernel": f"k_{dom}", "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
