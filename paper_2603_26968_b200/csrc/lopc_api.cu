@@ -162,8 +162,10 @@ int dev_info(DevInfo*& out) {
     CK(cudaEventCreateWithFlags(&g_dev.ev_join, cudaEventDisableTiming));
     CK(cudaDeviceGetAttribute(&g_dev.sms, cudaDevAttrMultiProcessorCount, dev));
     const int smem = (int)sizeof(EncSmem), dsmem = (int)sizeof(DecSmem);
-    CK(cudaFuncSetAttribute(k_encode<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    CK(cudaFuncSetAttribute(k_encode<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    CK(cudaFuncSetAttribute(k_encode<float, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    CK(cudaFuncSetAttribute(k_encode<float, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    CK(cudaFuncSetAttribute(k_encode<double, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    CK(cudaFuncSetAttribute(k_encode<double, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     CK(cudaFuncSetAttribute(k_decode, cudaFuncAttributeMaxDynamicSharedMemorySize, dsmem));
 #define QRA(TT, ND)                                                                                      \
   CK(cudaFuncSetAttribute(k_quant_flags<TT, ND, int32_t, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
@@ -575,6 +577,7 @@ int lopc_compress_ex(const void* in, int ndims, const uint64_t* dims, int dtype,
   ea.d0 = sh.d0;
   ea.d1 = sh.d1;
   ea.d2 = sh.d2;
+  set_escape_limits(ea, sh.dtype == LOPC_F64, eps);
   const size_t smem = sizeof(EncSmem);
   // The bin stream depends on x only: without per-kernel timing its CTAs run
   // on a side stream beside the (latency-bound) repair; the subbin CTAs follow
@@ -583,20 +586,13 @@ int lopc_compress_ex(const void* in, int ndims, const uint64_t* dims, int dtype,
   if (overlap) {
     CK(cudaEventRecord(di->ev_fork, st));
     CK(cudaStreamWaitEvent(di->side, di->ev_fork, 0));
-    ea.role = 1;
-    if (sh.dtype == LOPC_F32)
-      k_encode<float><<<(unsigned)sh.C, kCodecThreads, smem, di->side>>>(ea);
-    else
-      k_encode<double><<<(unsigned)sh.C, kCodecThreads, smem, di->side>>>(ea);
+    launch_encode(ea, sh.dtype == LOPC_F64, 1, (unsigned)sh.C, smem, di->side);
     CK(cudaGetLastError());
     CK(cudaEventRecord(di->ev_join, di->side));
   }
   if ((rc = run_repair(sh, x, eps, ws, L, st, tm, hc))) return rc;  // marks 3, 4
-  ea.role = overlap ? 2 : 0;
-  if (sh.dtype == LOPC_F32)
-    k_encode<float><<<(unsigned)(overlap ? sh.C : 2 * sh.C), kCodecThreads, smem, st>>>(ea);
-  else
-    k_encode<double><<<(unsigned)(overlap ? sh.C : 2 * sh.C), kCodecThreads, smem, st>>>(ea);
+  if (!overlap) launch_encode(ea, sh.dtype == LOPC_F64, 1, (unsigned)sh.C, smem, st);
+  launch_encode(ea, sh.dtype == LOPC_F64, 2, (unsigned)sh.C, smem, st);
   CK(cudaGetLastError());
   if (overlap) CK(cudaStreamWaitEvent(st, di->ev_join, 0));
   tm.mark();  // 5

@@ -189,29 +189,40 @@ __device__ __forceinline__ uint32_t level_down_warp(const uint8_t* bn, const uin
 // RZE_g encode of `in` (shared, 16-byte aligned, L bytes, zero up to the next
 // multiple of 16g) into `out` (shared, any alignment).  Returns the encoded
 // length; `out` is written only if that length <= limit.
-__device__ uint32_t rze_enc(const uint8_t* in, uint32_t L, int g, uint8_t* out, uint32_t limit, RzeScratch& R) {
+//
+// Only the first L_act bytes (a multiple of 16g, block-uniform) may be
+// non-zero: the bytes past them are taken as zero without being read (the
+// caller knows which bit planes are all zero), so only the units up to the
+// first all-zero one are visited.  L_act = L reads everything.
+__device__ uint32_t rze_enc(const uint8_t* in, uint32_t L, int g, uint8_t* out, uint32_t limit, RzeScratch& R,
+                            uint32_t L_act) {
   const int tid = threadIdx.x, lane = tid & 31;
   const uint32_t n = L / (uint32_t)g;
   uint32_t sz[6];
   const int top = rze_sizes(n, sz);
   const uint32_t units = (n + 15) / 16, ub = 16u * (uint32_t)g;
+  // units >= uact are all zero; unit uact still carries a B1 bit (B0 falls to 0)
+  const uint32_t uact = top == 0 ? units : min(units, L_act / ub);
+  const uint32_t uvis = min(units, uact + 1);
   constexpr int MAXIT = 5;  // units per thread: <= 1088 units / 256 threads
   uint32_t mk[MAXIT], rk[MAXIT];
   uint32_t running = 0;
-  const int iters = (int)((units + kCodecThreads - 1) / kCodecThreads);
+  const int iters = (int)((uvis + kCodecThreads - 1) / kCodecThreads);
+  if (top >= 1)  // B1 words past the visited units are zero
+    for (uint32_t t = (uint32_t)iters * (kCodecThreads / 16) + tid; t < (units + 15) / 16; t += kCodecThreads) R.b1[t] = 0;
 #pragma unroll
   for (int it = 0; it < MAXIT; ++it) {
     if (it >= iters) break;
     const uint32_t u = (uint32_t)(it * kCodecThreads + tid);
     uint32_t m = 0, prevb = 0;
-    if (u < units) {
+    if (u < uvis) {
       const uint8_t* p = in + u * ub;
-      m = nz_words8(p, g) | (nz_words8(p + 8 * g, g) << 8);
+      if (u < uact) m = nz_words8(p, g) | (nz_words8(p + 8 * g, g) << 8);
       prevb = u ? nz_words8(p - 8 * g, g) : 0u;
     }
     const uint32_t lo = m & 0xffu, hi = m >> 8;
     uint32_t b1 = 0;
-    if (top >= 1 && u < units) b1 = (uint32_t)(lo != prevb) | ((uint32_t)(hi != lo && 2 * u + 1 < sz[0]) << 1);
+    if (top >= 1 && u < uvis) b1 = (uint32_t)(lo != prevb) | ((uint32_t)(hi != lo && 2 * u + 1 < sz[0]) << 1);
     uint32_t tot;
     const uint32_t ex = block_scan_excl<uint32_t>((uint32_t)__popc(m) | ((uint32_t)__popc(b1) << 20), R.wsum, &tot);
     mk[it] = m | (b1 << 16);
@@ -219,7 +230,7 @@ __device__ uint32_t rze_enc(const uint8_t* in, uint32_t L, int g, uint8_t* out, 
     running += tot;
     if (top >= 1) {
       const uint32_t w = group_or(b1 << (2 * (u & 15)), 16);
-      if ((lane & 15) == 0 && u < units) R.b1[u >> 4] = w;
+      if ((lane & 15) == 0 && u < units) R.b1[u >> 4] = w;  // zero past uvis
     }
   }
   const uint32_t ndata = running & 0xfffffu, nk0 = running >> 20;
@@ -262,7 +273,7 @@ __device__ uint32_t rze_enc(const uint8_t* in, uint32_t L, int g, uint8_t* out, 
     for (int it = 0; it < MAXIT; ++it) {
       if (it >= iters) break;
       const uint32_t u = (uint32_t)(it * kCodecThreads + tid);
-      const bool valid = u < units;
+      const bool valid = u < uvis;
       const uint32_t m = valid ? mk[it] & 0xffffu : 0u, b1 = mk[it] >> 16;
       const uint32_t dr = rk[it] & 0xfffffu;
       if (valid) {
@@ -479,65 +490,20 @@ __host__ __device__ constexpr U nb_mask() {
   return (U)0xAAAAAAAAAAAAAAAAull;
 }
 
-// BIT_k (G20): words (swizzled shared) -> 8k planes of W bits (linear bytes),
-// run by threads [t0, t0 + nt).  With DIFF, word i is first replaced by
-// NB(w[i] - w[i-1]) (DIFFNB_k, G18/G19), computed on the fly.
-template <typename U, bool DIFF>
-__device__ __forceinline__ void bit_forward(const U* words, uint32_t* planes, int W, int t0, int nt) {
-  const int groups = W / 32;
-  for (int g = (int)threadIdx.x - t0; g >= 0 && g < groups; g += nt) {
-#pragma unroll
-    for (int half = 0; half < (int)sizeof(U) / 4; ++half) {
-      uint32_t A[32];
-      U prev = (DIFF && g) ? words[swz(32 * g - 1)] : (U)0;
-#pragma unroll
-      for (int i = 0; i < 32; ++i) {
-        U w = words[swz(32 * g + i)];
-        if (DIFF) {
-          const U cur = w;
-          w = (U)(((U)(cur - prev) + nb_mask<U>()) ^ nb_mask<U>());
-          prev = cur;
-        }
-        A[i] = (uint32_t)(w >> (32 * half));
-      }
-      transpose32(A);
-#pragma unroll
-      for (int j = 0; j < 32; ++j) planes[(32 * half + j) * groups + g] = A[j];
-    }
-  }
-}
-
-// inverse, by threads [t0, t0 + nt)
-template <typename U>
-__device__ __forceinline__ void bit_inverse(const uint32_t* planes, U* words, int W, int t0, int nt) {
-  const int groups = W / 32;
-  for (int g = (int)threadIdx.x - t0; g >= 0 && g < groups; g += nt) {
-#pragma unroll
-    for (int half = 0; half < (int)sizeof(U) / 4; ++half) {
-      uint32_t A[32];
-#pragma unroll
-      for (int j = 0; j < 32; ++j) A[j] = planes[(32 * half + j) * groups + g];
-      transpose32(A);
-#pragma unroll
-      for (int i = 0; i < 32; ++i) {
-        if (half == 0)
-          words[swz(32 * g + i)] = (U)A[i];
-        else
-          words[swz(32 * g + i)] |= (U)A[i] << (32 * half);
-      }
-    }
-  }
-}
-
-// In-place BIT_k / BIT_k^-1 on one shared buffer (words swizzled <-> planes
+// In-place BIT_k (G20) on one shared buffer (words swizzled -> planes
 // linear): every (group, 32-bit half) item is staged in registers, then the
-// block synchronises, then the results are stored.  All threads must call.
+// block synchronises, then the results are stored.  With DIFF, word i is
+// first replaced by NB(w[i] - w[i-1]) (DIFFNB_k, G18/G19), on the fly.
+// Returns P (block-uniform): planes >= P are all zero.  Only planes < P are
+// stored (rze_enc never reads past P planes: its L_act).  *pm is a zeroed
+// shared word.  All threads must call.
 template <typename U, bool DIFF>
-__device__ __forceinline__ void bit_forward_inplace(uint8_t* buf, int W) {
+__device__ __forceinline__ int bit_forward_inplace(uint8_t* buf, int W, unsigned long long* pm) {
   const int groups = W / 32, items = groups * (int)(sizeof(U) / 4);
   const int t = threadIdx.x, g = t % groups, half = t / groups;
   const U* words = reinterpret_cast<const U*>(buf);
   uint32_t A[32];
+  uint32_t orv = 0;
   if (t < items) {
     U prev = (DIFF && g) ? words[swz(32 * g - 1)] : (U)0;
 #pragma unroll
@@ -549,14 +515,61 @@ __device__ __forceinline__ void bit_forward_inplace(uint8_t* buf, int W) {
         prev = cur;
       }
       A[i] = (uint32_t)(w >> (32 * half));
+      orv |= A[i];
     }
     transpose32(A);
   }
+  // warps lie within one half (groups is a multiple of 32)
+  orv = __reduce_or_sync(0xffffffffu, orv);
+  if ((t & 31) == 0 && orv) atomicOr(pm, (unsigned long long)orv << (32 * (t < items ? half : 0)));
   __syncthreads();
+  const unsigned long long m = *pm;
+  const int P = m ? 64 - __clzll((long long)m) : 0;
   if (t < items) {
     uint32_t* planes = reinterpret_cast<uint32_t*>(buf);
 #pragma unroll
-    for (int j = 0; j < 32; ++j) planes[(32 * half + j) * groups + g] = A[j];
+    for (int j = 0; j < 32; ++j) {
+      if (32 * half + j >= P) break;
+      planes[(32 * half + j) * groups + g] = A[j];
+    }
+  }
+  __syncthreads();
+  return P;
+}
+
+// BIT_k of words whose planes >= P are zero, P <= 8 (the usual subbin
+// chunk: subbins are small): warp w transposes the groups [GPW w, GPW w + GPW)
+// with one warp ballot per (group, plane); lane k keeps the planes of group
+// GPW w + k, so the plane stores are conflict-free.  In place, all threads.
+template <typename U>
+__device__ __forceinline__ void bit_forward_ballot(uint8_t* buf, int W, int P) {
+  constexpr int NW = kCodecThreads / 32;
+  const int groups = W / 32, gpw = groups / NW;  // 16 (f32) / 8 (f64)
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const U* words = reinterpret_cast<const U*>(buf);
+  uint32_t m[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) m[j] = 0;
+#pragma unroll
+  for (int k = 0; k < 16; ++k) {
+    if (k >= gpw) break;
+    const int g = gpw * warp + k;
+    const uint32_t w = (uint32_t)words[swz(32 * g + lane)];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      if (j >= P) break;
+      const uint32_t v = __ballot_sync(0xffffffffu, (w >> j) & 1u);
+      m[j] = lane == k ? v : m[j];
+    }
+  }
+  __syncthreads();
+  uint32_t* planes = reinterpret_cast<uint32_t*>(buf);
+  if (lane < gpw) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      if (j >= P) break;
+      planes[j * groups + gpw * warp + lane] = m[j];
+    }
   }
   __syncthreads();
 }
@@ -598,8 +611,24 @@ struct EncodeArgs {
   float inv32;  // RN32(1/eps) for the f32 fast path, NaN = off
   int prof;     // diagnostic phase clocks
   uint64_t d0, d1, d2;
-  int role;     // 0: both streams (grid 2C); 1: bin CTAs only (grid C); 2: subbin CTAs only (grid C)
+  double xlim;   // |x| < xlim proves x regular (finite, |b| <= BINMAX): the subbin CTAs' escape test
+  float xlim32;  // the same bound as a float (f32 data)
 };
+
+// xlim = 2^30 eps (f32 data) / 2^49 eps (f64): |x| below it gives |x/eps| < 2^30
+// (2^49), so |b| <= 2^30 < BINMAX = 2^31 - 2 (|b| <= 2^49 < 2^50), and x is
+// finite.  xlim32 rounds 2^30 eps down to a float (FLT_MAX if larger; 0 if it
+// underflows, which only sends every point to the exact test).
+inline void set_escape_limits(EncodeArgs& ea, bool f64, double eps) {
+  ea.xlim = ldexp(eps, f64 ? 49 : 30);
+  const double l = ldexp(eps, 30);
+  float f = l >= 3.4028234663852886e38 ? 3.4028234663852886e38f : (float)l;
+  if ((double)f > l) f = nextafterf(f, 0.0f);
+  ea.xlim32 = f;
+}
+
+__device__ __forceinline__ bool surely_regular(float x, const EncodeArgs& a) { return fabsf(x) < a.xlim32; }
+__device__ __forceinline__ bool surely_regular(double x, const EncodeArgs& a) { return fabs(x) < a.xlim; }
 
 
 constexpr uint64_t kFlagAgg = 1ull << 62, kFlagIncl = 2ull << 62, kValMask = (1ull << 62) - 1;
@@ -639,41 +668,51 @@ __device__ __forceinline__ uint64_t lookback_warp(uint64_t* state, uint32_t c, u
 
 __device__ __forceinline__ uint32_t pad4(uint32_t v) { return (v + 3u) & ~3u; }
 
-// One CTA per (chunk, stream): blockIdx.x = 2c + role, role 0 = bins, 1 = subbins.
+// One CTA per (chunk, stream): k_encode<T, 1> encodes the bins of chunk
+// blockIdx.x, k_encode<T, 2> its subbins.
 struct EncSmem {
   alignas(16) uint8_t Wd[kChunkBytes + 64];  // words -> planes (in place) -> [subbins] payload
   alignas(16) uint8_t O[17408 + 128];        // [bins] payload | [subbins] a4 queue, RZE_k output
   RzeScratch R;
+  unsigned long long pm[2];                  // OR of the words (subbins) / plane mask of BIT
   uint32_t misc[4];
 };
 
-template <typename T>
+template <typename T, int ROLE>
 __global__ void __launch_bounds__(kCodecThreads, 6) k_encode(EncodeArgs a) {
   using U = typename VT<T>::U;
   using I = typename VT<T>::I;
+  constexpr bool SUBS = ROLE == 2;
   constexpr int K = VT<T>::K;
   constexpr int W = kChunkBytes / K;
   constexpr int PER = W / kCodecThreads;  // words per thread (16 f32, 8 f64)
+  constexpr int PB = W / 8;               // bytes per bit plane
   extern __shared__ __align__(16) uint8_t smem_raw[];
   EncSmem& sm = *reinterpret_cast<EncSmem*>(smem_raw);
   U* WD = reinterpret_cast<U*>(sm.Wd);
   uint16_t* Q = reinterpret_cast<uint16_t*>(sm.O);
   const int tid = threadIdx.x, lane = tid & 31;
-  const uint32_t c = a.role ? blockIdx.x : blockIdx.x >> 1;
-  const bool subs = a.role ? a.role == 2 : (blockIdx.x & 1);
+  const uint32_t c = blockIdx.x;
   PhaseClock pc;
   pc.start(a.prof);
-  if (tid == 0) sm.misc[0] = 0;  // a4 queue length
+  if (tid == 0) {
+    sm.misc[0] = 0;  // a4 queue length
+    sm.pm[0] = 0;
+    sm.pm[1] = 0;
+  }
   const uint64_t e0 = (uint64_t)c * W;
   const uint32_t cnt = (uint32_t)min((uint64_t)W, a.n - e0);
   const T* X = static_cast<const T*>(a.x) + e0;
   const uint32_t* S = a.s + e0;
   __syncthreads();
 
-  // --- a1: re-quantize; bin words (role 0) or subbin words + a4 queue (role 1).
-  // Thread slot k = 4v + q holds element 4 (v * NT + tid) + q.
+  // --- a1: re-quantize; bin words (ROLE 1) or subbin words + a4 queue (ROLE 2).
+  // Thread slot k = 4v + q holds element 4 (v * NT + tid) + q.  Elements past
+  // the chunk's end load as x = 0, s = 0, whose words are 0 (b(0) = 0), the
+  // zero padding of G23.
   constexpr int NV = PER / 2;  // two halves of PER slots (register budget)
-  uint32_t escm = 0, qmask = 0;
+  uint32_t qmask = 0, nesc = 0;
+  U orw = 0;
 #pragma unroll 1
   for (int hh = 0; hh < 2; ++hh) {
     T xs[NV];
@@ -690,7 +729,7 @@ __global__ void __launch_bounds__(kCodecThreads, 6) k_encode(EncodeArgs a) {
           const double2 x1 = __ldg(reinterpret_cast<const double2*>(X + i0 + 2));
           xs[4 * v] = x0.x, xs[4 * v + 1] = x0.y, xs[4 * v + 2] = x1.x, xs[4 * v + 3] = x1.y;
         }
-        if (subs) {
+        if constexpr (SUBS) {
           const uint4 sv = __ldg(reinterpret_cast<const uint4*>(S + i0));
           ss[4 * v] = sv.x, ss[4 * v + 1] = sv.y, ss[4 * v + 2] = sv.z, ss[4 * v + 3] = sv.w;
         }
@@ -701,42 +740,55 @@ __global__ void __launch_bounds__(kCodecThreads, 6) k_encode(EncodeArgs a) {
         const int i = 4 * ((hh * (NV / 4) + (k >> 2)) * kCodecThreads + tid) + (k & 3);
         const bool in = (uint32_t)i < cnt;
         xs[k] = in ? X[i] : (T)0;
-        ss[k] = (in && subs) ? S[i] : 0u;
+        if constexpr (SUBS) ss[k] = in ? S[i] : 0u;
       }
     }
 #pragma unroll
-    for (int v = 0; v < NV / 4; ++v) {  // groups of 4: fast attempt, rare exact fix-up, words
-      I bb[4];
-      uint32_t slow = 0;
+    for (int v = 0; v < NV / 4; ++v) {
+      U wv[4];
+      if constexpr (!SUBS) {  // fast attempt, rare exact fix-up (near a half-integer, escapes, huge bins)
+        I bb[4];
+        uint32_t slow = 0;
 #pragma unroll
-      for (int q = 0; q < 4; ++q) slow |= (uint32_t)!qtry(xs[4 * v + q], a.inv32, a.inv, bb[q]) << q;
-      if (slow) {  // rare: near a half-integer, escapes, huge bins
+        for (int q = 0; q < 4; ++q) slow |= (uint32_t)!qtry(xs[4 * v + q], a.inv32, a.inv, bb[q]) << q;
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          if ((slow >> q) & 1u) {
-            const int64_t r = quantize_slow<T>(xs[4 * v + q], a.eps, a.inv);
-            if (r == kEscape) escm |= 1u << (hh * NV + 4 * v + q);
-            bb[q] = (I)r;
+        for (int q = 0; q < 4; ++q) wv[q] = (U)bb[q];
+        if (slow) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            if ((slow >> q) & 1u) {
+              const int64_t r = quantize_slow<T>(xs[4 * v + q], a.eps, a.inv);
+              nesc += r == kEscape;
+              wv[q] = r == kEscape ? VT<T>::kSentinel : (U)(I)r;
+            }
           }
         }
+      } else {  // escape test only: |x| < xlim proves the point regular
+        uint32_t slow = 0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          slow |= (uint32_t)!surely_regular(xs[4 * v + q], a) << q;
+          wv[q] = (U)ss[4 * v + q];
+        }
+        if (slow) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if (((slow >> q) & 1u) && quantize_slow<T>(xs[4 * v + q], a.eps, a.inv) == kEscape) {
+              wv[q] = (U)as_bits(xs[4 * v + q]);
+              ss[4 * v + q] = 0;  // not queued for a4
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          qmask |= (uint32_t)(ss[4 * v + q] != 0) << (hh * NV + 4 * v + q);
+          orw |= wv[q];
+        }
       }
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int k = 4 * v + q, kk = hh * NV + k;
-        const int i = 4 * ((hh * (NV / 4) + v) * kCodecThreads + tid) + q;
-        const bool in = (uint32_t)i < cnt, e = (escm >> kk) & 1u;
-        U w;
-        if (subs) {
-          w = e ? (U)as_bits(xs[k]) : (U)ss[k];
-          qmask |= (uint32_t)(!e && ss[k] != 0) << kk;
-        } else {
-          w = e ? VT<T>::kSentinel : (U)bb[q];
-        }
-        WD[swz(i)] = in ? w : (U)0;
-      }
+      for (int q = 0; q < 4; ++q) WD[swz(4 * ((hh * (NV / 4) + v) * kCodecThreads + tid) + q)] = wv[q];
     }
   }
-  if (subs) {  // a4 queue: one warp scan per thread-mask
+  if constexpr (SUBS) {  // a4 queue: one warp scan per thread-mask; OR of the words
     const uint32_t nq = __popc(qmask);
     uint32_t incl = nq;
 #pragma unroll
@@ -751,15 +803,18 @@ __global__ void __launch_bounds__(kCodecThreads, 6) k_encode(EncodeArgs a) {
       const int k = __ffs(m) - 1;
       Q[base++] = (uint16_t)(4 * ((k >> 2) * kCodecThreads + tid) + (k & 3));
     }
+    const uint32_t olo = __reduce_or_sync(0xffffffffu, (uint32_t)orw);
+    const uint32_t ohi = sizeof(U) == 8 ? __reduce_or_sync(0xffffffffu, (uint32_t)((uint64_t)orw >> 32)) : 0u;
+    if (lane == 0 && (olo | ohi)) atomicOr(&sm.pm[0], ((unsigned long long)ohi << 32) | olo);
   } else {
-    const uint32_t esc = __reduce_add_sync(0xffffffffu, (uint32_t)__popc(escm));
+    const uint32_t esc = __reduce_add_sync(0xffffffffu, nesc);
     if (lane == 0 && esc) atomicAdd(&a.ctr->escapes, (unsigned long long)esc);
   }
   __syncthreads();
   pc.mark(a.ctr, 1);
 
   uint32_t size;
-  if (subs) {
+  if constexpr (SUBS) {
     // --- a4: bound self-check of the queued points: key(lo(b)) + s <= key(x)
     const uint32_t nq = sm.misc[0];
     uint32_t bad = 0;
@@ -774,13 +829,18 @@ __global__ void __launch_bounds__(kCodecThreads, 6) k_encode(EncodeArgs a) {
     if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(&a.ctr->err, kErrBound);
     pc.mark(a.ctr, 2);
     // --- a6: subbins: BIT_k -> RZE_k -> RZE_1 ----------------------
-    bit_forward_inplace<U, false>(sm.Wd, W);
+    const unsigned long long ow = sm.pm[0];
+    int P = ow ? 64 - __clzll((long long)ow) : 0;
+    if (P <= 8)
+      bit_forward_ballot<U>(sm.Wd, W, P);
+    else
+      P = bit_forward_inplace<U, false>(sm.Wd, W, &sm.pm[1]);
     pc.mark(a.ctr, 3);
-    const uint32_t l1 = rze_enc(sm.Wd, kChunkBytes, K, sm.O, 0xffffffffu, sm.R);
+    const uint32_t l1 = rze_enc(sm.Wd, kChunkBytes, K, sm.O, 0xffffffffu, sm.R, (uint32_t)P * PB);
     for (uint32_t t = l1 + tid; t < ((l1 + 15) & ~15u) + 16; t += kCodecThreads) sm.O[t] = 0;
     __syncthreads();
     pc.mark(a.ctr, 5);
-    const uint32_t l2 = rze_enc(sm.O, l1, 1, sm.Wd + 2, kChunkBytes - 6, sm.R);
+    const uint32_t l2 = rze_enc(sm.O, l1, 1, sm.Wd + 2, kChunkBytes - 6, sm.R, (l1 + 15) & ~15u);
     size = l2 <= kChunkBytes - 6 ? pad4(2 + l2) : kChunkBytes;
     if (size < kChunkBytes) {
       if (tid == 0) {
@@ -792,9 +852,9 @@ __global__ void __launch_bounds__(kCodecThreads, 6) k_encode(EncodeArgs a) {
     pc.mark(a.ctr, 6);
   } else {
     // --- a5: bins: DIFFNB_k -> BIT_k -> RZE_1 -------------------
-    bit_forward_inplace<U, true>(sm.Wd, W);
+    const int P = bit_forward_inplace<U, true>(sm.Wd, W, &sm.pm[1]);
     pc.mark(a.ctr, 3);
-    const uint32_t l = rze_enc(sm.Wd, kChunkBytes, 1, sm.O, kChunkBytes - 4, sm.R);
+    const uint32_t l = rze_enc(sm.Wd, kChunkBytes, 1, sm.O, kChunkBytes - 4, sm.R, (uint32_t)P * PB);
     size = l <= kChunkBytes - 4 ? pad4(l) : kChunkBytes;
     if (size < kChunkBytes && (uint32_t)tid < size - l) sm.O[l + tid] = 0;
     pc.mark(a.ctr, 4);
@@ -804,10 +864,10 @@ __global__ void __launch_bounds__(kCodecThreads, 6) k_encode(EncodeArgs a) {
   // --- a7 (part 1): the payload goes to this chunk's staging slot (bins at
   // +0, subbins at +16 KiB); k_chunk_scan + k_place put it in the stream.
   if (tid == 0) {
-    a.sizes[2 * c + (subs ? 1 : 0)] = size;
-    atomicAdd(subs ? &a.ctr->sub_bytes : &a.ctr->bin_bytes, (unsigned long long)size);
+    a.sizes[2 * c + (SUBS ? 1 : 0)] = size;
+    atomicAdd(SUBS ? &a.ctr->sub_bytes : &a.ctr->bin_bytes, (unsigned long long)size);
   }
-  uint32_t* dst = reinterpret_cast<uint32_t*>(a.stage + (size_t)c * 2 * kChunkBytes + (subs ? kChunkBytes : 0));
+  uint32_t* dst = reinterpret_cast<uint32_t*>(a.stage + (size_t)c * 2 * kChunkBytes + (SUBS ? kChunkBytes : 0));
   if (size == kChunkBytes) {
     // raw fallback (G23): rebuild the words (the buffer now holds planes)
     for (int i = tid; i < W; i += kCodecThreads) {
@@ -815,20 +875,29 @@ __global__ void __launch_bounds__(kCodecThreads, 6) k_encode(EncodeArgs a) {
       if ((uint32_t)i < cnt) {
         I b;
         if (quantize_fast<T>(X[i], a.inv32, a.eps, a.inv, b))
-          w = subs ? (U)S[i] : (U)b;
+          w = SUBS ? (U)S[i] : (U)b;
         else
-          w = subs ? (U)as_bits(X[i]) : VT<T>::kSentinel;
+          w = SUBS ? (U)as_bits(X[i]) : VT<T>::kSentinel;
       }
 #pragma unroll
       for (int h = 0; h < K / 4; ++h) dst[i * (K / 4) + h] = (uint32_t)(w >> (32 * h));
     }
   } else {
-    const uint4* src = reinterpret_cast<const uint4*>(subs ? sm.Wd : sm.O);
+    const uint4* src = reinterpret_cast<const uint4*>(SUBS ? sm.Wd : sm.O);
     uint4* d4 = reinterpret_cast<uint4*>(dst);
     for (uint32_t i = tid; i < (size + 15) / 16; i += kCodecThreads) d4[i] = src[i];
   }
   __syncthreads();
   pc.mark(a.ctr, 7);
+}
+
+// Host: one k_encode grid of C CTAs for one stream (role 1 bins, 2 subbins).
+inline void launch_encode(const EncodeArgs& ea, bool f64, int role, unsigned C, size_t smem, cudaStream_t st) {
+  if (C == 0) return;
+  if (!f64)
+    (role == 1 ? k_encode<float, 1> : k_encode<float, 2>)<<<C, kCodecThreads, smem, st>>>(ea);
+  else
+    (role == 1 ? k_encode<double, 1> : k_encode<double, 2>)<<<C, kCodecThreads, smem, st>>>(ea);
 }
 
 // ---------------------------------------------------------------------------

@@ -188,11 +188,10 @@ struct Slab {
     ea.d0 = g.d0;
     ea.d1 = g.d1;
     ea.d2 = g.d2;
+    set_escape_limits(ea, g.dtype == LOPC_F64, eps);
     const size_t smem = sizeof(EncSmem);
-    if (g.dtype == LOPC_F32)
-      k_encode<float><<<(unsigned)(2 * geo.C_local), kCodecThreads, smem, st>>>(ea);
-    else
-      k_encode<double><<<(unsigned)(2 * geo.C_local), kCodecThreads, smem, st>>>(ea);
+    launch_encode(ea, g.dtype == LOPC_F64, 1, (unsigned)geo.C_local, smem, st);
+    launch_encode(ea, g.dtype == LOPC_F64, 2, (unsigned)geo.C_local, smem, st);
     CK(cudaGetLastError());
     if (tm) tm->mark();
     ScanArgs sa{};
