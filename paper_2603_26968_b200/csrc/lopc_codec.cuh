@@ -331,20 +331,24 @@ __device__ uint32_t rze_enc(const uint8_t* in, uint32_t L, int g, uint8_t* out, 
 // reconstructs L bytes into `out` (shared, 16-byte aligned, room for L
 // rounded up to 16g).  Returns the payload bytes consumed, or 0xffffffff if
 // the payload is too short for what its bitmaps announce (corrupt).
-__device__ uint32_t rze_dec(const uint8_t* in, uint32_t in_len, uint32_t L, int g, uint8_t* out, RzeScratch& R) {
+//
+// align = 0: all L bytes are written.  align > 0 (a multiple of 16g): B0 is
+// zero past its last change when the last K0 byte is 0, so the units past
+// it are all zero; only the bytes up to the next multiple of `align` after
+// them are written (the rest of `out` is left as it was) and *act returns
+// that length — the caller's bit planes past *act are zero.
+__device__ uint32_t rze_dec(const uint8_t* in, uint32_t in_len, uint32_t L, int g, uint8_t* out, RzeScratch& R,
+                            uint32_t align, uint32_t* act) {
   const int tid = threadIdx.x;
   const uint32_t n = L / (uint32_t)g;
   uint32_t sz[6];
   const int top = rze_sizes(n, sz);
   const uint32_t units = (n + 15) / 16, ub = 16u * (uint32_t)g;
-  if (g != 1) {  // words without data stay 0 (the scatter below writes only the others)
-    uint4* o4 = reinterpret_cast<uint4*>(out);
-    for (uint32_t t = tid; t < units * ub / 16; t += kCodecThreads) o4[t] = make_uint4(0, 0, 0, 0);
-  }
   if (tid < 32) {
     const int lane = tid;
     bool ok = sz[top] <= in_len;
     uint32_t pos = sz[top];
+    uint32_t uact = units;
     uint8_t* b1 = reinterpret_cast<uint8_t*>(R.b1);
     uint8_t* b2 = reinterpret_cast<uint8_t*>(R.b2);
     uint8_t* b3 = reinterpret_cast<uint8_t*>(R.b3);
@@ -364,9 +368,10 @@ __device__ uint32_t rze_dec(const uint8_t* in, uint32_t in_len, uint32_t L, int 
         ok = ok && pos <= in_len;
         __syncwarp();
       }
-      // exclusive popcount prefix of B1 words, bits < sz0 only
+      // exclusive popcount prefix of B1 words, bits < sz0 only; last set bit
       const uint32_t nw1 = (sz[0] + 31) / 32;
       uint32_t carry = 0;
+      int last = -1;
       for (uint32_t base = 0; base < nw1; base += 32) {
         const uint32_t w = base + lane;
         uint32_t c = 0;
@@ -376,6 +381,7 @@ __device__ uint32_t rze_dec(const uint8_t* in, uint32_t in_len, uint32_t L, int 
           if (sz[0] - 32 * w < 32) word &= (1u << (sz[0] - 32 * w)) - 1u;
           R.b1[w] = word;
           c = __popc(word);
+          if (word) last = (int)(32 * w) + 31 - __clz(word);
         }
         uint32_t incl = c;
 #pragma unroll
@@ -386,14 +392,18 @@ __device__ uint32_t rze_dec(const uint8_t* in, uint32_t in_len, uint32_t L, int 
         if (w < nw1) R.pre1[w] = carry + incl - c;
         carry += __shfl_sync(0xffffffffu, incl, 31);
       }
+      last = __reduce_max_sync(0xffffffffu, last);
       const uint32_t koff = pos;
       pos += carry;  // |K0|
       ok = ok && pos <= in_len;
+      // B0[t] = B0[last] for t >= last; when that byte is 0, units >= ceil(last / 2) are zero
+      if (ok && align) uact = last < 0 ? 0u : (in[pos - 1] == 0 ? ((uint32_t)last + 1) / 2 : units);
       if (lane == 0) R.info[0] = koff;
     }
     if (lane == 0) {
       R.info[1] = top == 0 ? sz[0] : pos;
       R.info[2] = ok;
+      R.info[3] = uact;
     }
   }
   __syncthreads();
@@ -401,9 +411,14 @@ __device__ uint32_t rze_dec(const uint8_t* in, uint32_t in_len, uint32_t L, int 
     __syncthreads();
     return 0xffffffffu;
   }
-  const uint32_t koff = R.info[0], doff = R.info[1];
+  const uint32_t koff = R.info[0], doff = R.info[1], uact = R.info[3];
+  // bytes written: the active units, then zeros up to the alignment
+  const uint32_t wend = align ? min(units * ub, (uact * ub + align - 1) / align * align) : units * ub;
+  for (uint32_t t = uact * ub / 16 + tid; t < wend / 16; t += kCodecThreads)
+    reinterpret_cast<uint4*>(out)[t] = make_uint4(0, 0, 0, 0);
+  if (act) *act = wend;
   constexpr int MAXIT = 5;
-  const int iters = (int)((units + kCodecThreads - 1) / kCodecThreads);
+  const int iters = (int)((uact + kCodecThreads - 1) / kCodecThreads);
   uint32_t running = 0;
   bool bad = false;
 #pragma unroll
@@ -411,7 +426,7 @@ __device__ uint32_t rze_dec(const uint8_t* in, uint32_t in_len, uint32_t L, int 
     if (it >= iters) break;
     const uint32_t u = (uint32_t)(it * kCodecThreads + tid);
     uint32_t m = 0;
-    if (u < units) {
+    if (u < uact) {
       uint32_t lo, hi;
       const uint32_t t0 = 2 * u, t1 = 2 * u + 1;
       if (top == 0) {
@@ -431,7 +446,7 @@ __device__ uint32_t rze_dec(const uint8_t* in, uint32_t in_len, uint32_t L, int 
     uint32_t dr = running + block_scan_excl<uint32_t>((uint32_t)__popc(m), R.wsum, &tot);
     running += tot;
     if (doff + (uint32_t)g * running > in_len) bad = true;  // block-uniform
-    if (!bad && g == 1 && u < units) {
+    if (!bad && g == 1 && u < uact) {
       const uint8_t* src = in + doff;
       uint8_t* dst = out + u * ub;
       uint32_t w4[4] = {0, 0, 0, 0};
@@ -440,25 +455,31 @@ __device__ uint32_t rze_dec(const uint8_t* in, uint32_t in_len, uint32_t L, int 
         if ((m >> j) & 1u) w4[j >> 2] |= (uint32_t)src[dr++] << (8 * (j & 3));
       *reinterpret_cast<uint4*>(dst) = make_uint4(w4[0], w4[1], w4[2], w4[3]);
     } else if (!bad && g != 1) {
-      // g = 4 / 8: `out` was zeroed up front; units with data are written one
-      // at a time per warp, their words spread over the lanes (conflict-free)
+      // g = 4 / 8: units without data are zeroed by their thread; units with
+      // data are written one at a time per warp, their words spread over the
+      // lanes (conflict-free)
       const int lane = tid & 31;
       const int uwl = g == 4 ? 0 : 1;
       const int pu = 16 << uwl;
       const uint8_t* src = in + doff;
       uint32_t* out32 = reinterpret_cast<uint32_t*>(out);
-      const uint32_t mm = u < units ? m : 0u;
+      if (u < uact && m == 0) {
+        uint4* o4 = reinterpret_cast<uint4*>(out + u * ub);
+        for (int q = 0; q < pu / 4; ++q) o4[q] = make_uint4(0, 0, 0, 0);
+      }
+      const uint32_t mm = u < uact ? m : 0u;
       for (uint32_t nzl = __ballot_sync(0xffffffffu, mm != 0); nzl; nzl &= nzl - 1) {
         const int l = __ffs(nzl) - 1;
         const uint32_t mu = __shfl_sync(0xffffffffu, mm, l), du = __shfl_sync(0xffffffffu, dr, l);
         const uint32_t uu = u - lane + l;
         if (lane < pu) {
           const int j = lane >> uwl, hh = lane & ((1 << uwl) - 1);
+          uint32_t v = 0;
           if ((mu >> j) & 1u) {
             const uint8_t* b = src + (size_t)(du + __popc(mu & ((1u << j) - 1u))) * g + 4 * hh;
-            out32[uu * pu + lane] =
-                (uint32_t)b[0] | ((uint32_t)b[1] << 8) | ((uint32_t)b[2] << 16) | ((uint32_t)b[3] << 24);
+            v = (uint32_t)b[0] | ((uint32_t)b[1] << 8) | ((uint32_t)b[2] << 16) | ((uint32_t)b[3] << 24);
           }
+          out32[uu * pu + lane] = v;
         }
       }
     }
@@ -541,48 +562,61 @@ __device__ __forceinline__ int bit_forward_inplace(uint8_t* buf, int W, unsigned
 // chunk: subbins are small): warp w transposes the groups [GPW w, GPW w + GPW)
 // with one warp ballot per (group, plane); lane k keeps the planes of group
 // GPW w + k, so the plane stores are conflict-free.  In place, all threads.
-template <typename U>
-__device__ __forceinline__ void bit_forward_ballot(uint8_t* buf, int W, int P) {
+template <typename U, int P>
+__device__ __forceinline__ void bit_forward_ballot_p(uint8_t* buf, int W) {
   constexpr int NW = kCodecThreads / 32;
   const int groups = W / 32, gpw = groups / NW;  // 16 (f32) / 8 (f64)
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const U* words = reinterpret_cast<const U*>(buf);
-  uint32_t m[8];
+  uint32_t m[P > 0 ? P : 1];
 #pragma unroll
-  for (int j = 0; j < 8; ++j) m[j] = 0;
+  for (int j = 0; j < P; ++j) m[j] = 0;
 #pragma unroll
   for (int k = 0; k < 16; ++k) {
-    if (k >= gpw) break;
-    const int g = gpw * warp + k;
-    const uint32_t w = (uint32_t)words[swz(32 * g + lane)];
+    if (k < gpw) {
+      const uint32_t w = (uint32_t)words[swz(32 * (gpw * warp + k) + lane)];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      if (j >= P) break;
-      const uint32_t v = __ballot_sync(0xffffffffu, (w >> j) & 1u);
-      m[j] = lane == k ? v : m[j];
+      for (int j = 0; j < P; ++j) {
+        const uint32_t v = __ballot_sync(0xffffffffu, (w & (1u << j)) != 0u);
+        m[j] = lane == k ? v : m[j];
+      }
     }
   }
   __syncthreads();
   uint32_t* planes = reinterpret_cast<uint32_t*>(buf);
   if (lane < gpw) {
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      if (j >= P) break;
-      planes[j * groups + gpw * warp + lane] = m[j];
-    }
+    for (int j = 0; j < P; ++j) planes[j * groups + gpw * warp + lane] = m[j];
   }
   __syncthreads();
 }
 
 template <typename U>
-__device__ __forceinline__ void bit_inverse_inplace(uint8_t* buf, int W) {
+__device__ __forceinline__ void bit_forward_ballot(uint8_t* buf, int W, int P) {
+  switch (P) {
+    case 0: bit_forward_ballot_p<U, 0>(buf, W); break;
+    case 1: bit_forward_ballot_p<U, 1>(buf, W); break;
+    case 2: bit_forward_ballot_p<U, 2>(buf, W); break;
+    case 3: bit_forward_ballot_p<U, 3>(buf, W); break;
+    case 4: bit_forward_ballot_p<U, 4>(buf, W); break;
+    case 5: bit_forward_ballot_p<U, 5>(buf, W); break;
+    case 6: bit_forward_ballot_p<U, 6>(buf, W); break;
+    case 7: bit_forward_ballot_p<U, 7>(buf, W); break;
+    default: bit_forward_ballot_p<U, 8>(buf, W); break;
+  }
+}
+
+// Inverse BIT_k in place (planes linear -> words swizzled); planes >= P are
+// zero and not read.  All threads must call.
+template <typename U>
+__device__ __forceinline__ void bit_inverse_inplace(uint8_t* buf, int W, int P) {
   const int groups = W / 32, items = groups * (int)(sizeof(U) / 4);
   const int t = threadIdx.x, g = t % groups, half = t / groups;
   uint32_t A[32];
   if (t < items) {
     const uint32_t* planes = reinterpret_cast<const uint32_t*>(buf);
 #pragma unroll
-    for (int j = 0; j < 32; ++j) A[j] = planes[(32 * half + j) * groups + g];
+    for (int j = 0; j < 32; ++j) A[j] = 32 * half + j < P ? planes[(32 * half + j) * groups + g] : 0u;
     transpose32(A);
   }
   __syncthreads();
@@ -592,6 +626,44 @@ __device__ __forceinline__ void bit_inverse_inplace(uint8_t* buf, int W) {
     for (int i = 0; i < 32; ++i) w32[swz(32 * g + i) * (int)(sizeof(U) / 4) + half] = A[i];
   }
   __syncthreads();
+}
+
+// The same for P <= 3 (the usual subbin chunk) without transposes: lane l of
+// warp w builds word 32 g + l of its groups g from bit l of the P plane words
+// (broadcast loads).  All threads must call.
+template <typename U, int P>
+__device__ __forceinline__ void bit_inverse_small_p(uint8_t* buf, int W) {
+  constexpr int NW = kCodecThreads / 32;
+  const int groups = W / 32, gpw = groups / NW;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t* planes = reinterpret_cast<const uint32_t*>(buf);
+  uint32_t wv[16];
+#pragma unroll
+  for (int k = 0; k < 16; ++k) {
+    wv[k] = 0;
+    if (k < gpw) {
+      const int g = gpw * warp + k;
+#pragma unroll
+      for (int j = 0; j < P; ++j) wv[k] |= ((planes[j * groups + g] >> lane) << j) & (1u << j);
+    }
+  }
+  __syncthreads();
+  U* words = reinterpret_cast<U*>(buf);
+#pragma unroll
+  for (int k = 0; k < 16; ++k)
+    if (k < gpw) words[swz(32 * (gpw * warp + k) + lane)] = (U)wv[k];
+  __syncthreads();
+}
+
+template <typename U>
+__device__ __forceinline__ void bit_inverse_planes(uint8_t* buf, int W, int P) {
+  switch (P) {
+    case 0: bit_inverse_small_p<U, 0>(buf, W); break;
+    case 1: bit_inverse_small_p<U, 1>(buf, W); break;
+    case 2: bit_inverse_small_p<U, 2>(buf, W); break;
+    case 3: bit_inverse_small_p<U, 3>(buf, W); break;
+    default: bit_inverse_inplace<U>(buf, W, P); break;
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -1119,6 +1191,7 @@ struct DecSmem {
   alignas(16) uint8_t O[17408 + 128];        // payload (bins) | RZE_1^-1 output (subbins)
   RzeScratch R;
   uint32_t bad, ticket;
+  int tmin, tmax;  // bin range of the half being reconstructed (f32 lo-key table)
 };
 
 // Copy `len` payload bytes (global, 4-aligned) into shared memory and zero
@@ -1148,10 +1221,12 @@ __device__ __noinline__ void decode_stream(const DecodeArgs& a, const uint8_t* p
     pc.mark(a.ctr, subs ? 10 : 9);
     return;
   }
+  constexpr uint32_t PB = W / 8;  // bytes per bit plane
+  uint32_t act = kChunkBytes;     // planes past act / PB are zero (and not written)
   if (!subs) {
     load_payload(p, size, sm.O);
     __syncthreads();
-    const uint32_t used = rze_dec(sm.O, size, kChunkBytes, 1, sm.Wd, sm.R);
+    const uint32_t used = rze_dec(sm.O, size, kChunkBytes, 1, sm.Wd, sm.R, PB, &act);
     if (used == 0xffffffffu || pad4(used) != size) bad = true;
   } else {
     load_payload(p, size, sm.Wd);
@@ -1160,11 +1235,11 @@ __device__ __noinline__ void decode_stream(const DecodeArgs& a, const uint8_t* p
     const uint32_t l1max = kChunkBytes + kChunkBytes / K / 8 + 64 + 8;
     if (l1 > l1max || size < 2) bad = true;
     if (!bad) {
-      const uint32_t used = rze_dec(sm.Wd + 2, size - 2, l1, 1, sm.O, sm.R);
+      const uint32_t used = rze_dec(sm.Wd + 2, size - 2, l1, 1, sm.O, sm.R, 0, nullptr);
       if (used == 0xffffffffu || pad4(2 + used) != size) bad = true;
     }
     if (!bad) {
-      const uint32_t used2 = rze_dec(sm.O, l1, kChunkBytes, K, sm.Wd, sm.R);
+      const uint32_t used2 = rze_dec(sm.O, l1, kChunkBytes, K, sm.Wd, sm.R, PB, &act);
       if (used2 != l1) bad = true;
     }
   }
@@ -1177,7 +1252,7 @@ __device__ __noinline__ void decode_stream(const DecodeArgs& a, const uint8_t* p
     __syncthreads();
     return;
   }
-  bit_inverse_inplace<U>(sm.Wd, W);
+  bit_inverse_planes<U>(sm.Wd, W, (int)(act / PB));
   pc.mark(a.ctr, 11);
   if (!subs) {  // NB^-1 + prefix sum (thread owns PER consecutive words)
     U d[PER];
@@ -1212,7 +1287,7 @@ __device__ __noinline__ void decode_stream(const DecodeArgs& a, const uint8_t* p
 // repetitive), and the values leave as 16-byte stores.
 template <typename T>
 __device__ __forceinline__ void reconstruct_half(const DecodeArgs& a, const Hdr& h, uint32_t c, int r, const uint8_t* wb,
-                                                 int wb_off, const uint8_t* ws, int ws_off) {
+                                                 int wb_off, const uint8_t* ws, int ws_off, DecSmem& sm) {
   using U = typename VT<T>::U;
   using I = typename VT<T>::I;
   constexpr int W = kChunkBytes / VT<T>::K;
@@ -1229,22 +1304,48 @@ __device__ __forceinline__ void reconstruct_half(const DecodeArgs& a, const Hdr&
     swv[v] = SW[swz(i0 + v - ws_off)];
   }
   U out[PER];
-  U pb = VT<T>::kSentinel;
-  int64_t pk = 0;
+  if constexpr (sizeof(U) == 4) {
+    // f32: key(lo(b)) for every bin of the half in a shared table when the
+    // half's bin range is small (the usual case: bins are locally smooth),
+    // else per element; the same lo_key32_nb either way
+    constexpr int kTab = 2048;  // entries at sm.O + 8 KiB (the partner's half copy is below)
+    int lmin = INT_MAX, lmax = INT_MIN;
 #pragma unroll
-  for (int v = 0; v < PER; ++v) {
-    const U bw = bwv[v];
-    if (bw != pb && bw != VT<T>::kSentinel) {
-      pk = (int64_t)lo_key<T>((int64_t)(I)bw, h.eps);
-      pb = bw;
+    for (int v = 0; v < PER; ++v)
+      if (bwv[v] != VT<T>::kSentinel) {
+        lmin = min(lmin, (int)bwv[v]);
+        lmax = max(lmax, (int)bwv[v]);
+      }
+    lmin = __reduce_min_sync(0xffffffffu, lmin);
+    lmax = __reduce_max_sync(0xffffffffu, lmax);
+    if ((threadIdx.x & 31) == 0) {
+      atomicMin(&sm.tmin, lmin);
+      atomicMax(&sm.tmax, lmax);
     }
-    const int64_t k = pk + (int64_t)swv[v];
-    U bits;
-    if constexpr (sizeof(U) == 4)
-      bits = bits_of_key32(k);
-    else
-      bits = bits_of_key64(k);
-    out[v] = bw == VT<T>::kSentinel ? swv[v] : bits;
+    __syncthreads();
+    const int tmin = sm.tmin;
+    const int64_t R = (int64_t)sm.tmax - (int64_t)tmin + 1;
+    int32_t* tab = reinterpret_cast<int32_t*>(sm.O + kChunkBytes / 2);
+    const bool use_tab = R > 0 && R <= kTab;
+    if (use_tab) {
+      for (int k = threadIdx.x; k < (int)R; k += kCodecThreads) tab[k] = lo_key32_nb(tmin + k, h.eps);
+      __syncthreads();
+    }
+#pragma unroll
+    for (int v = 0; v < PER; ++v) {
+      const U bw = bwv[v];
+      const bool esc = bw == VT<T>::kSentinel;
+      const int32_t lk = use_tab ? tab[esc ? 0 : (int)bw - tmin] : lo_key32_nb((int32_t)bw, h.eps);
+      const uint32_t k = (uint32_t)lk + (uint32_t)swv[v];  // wraps only for escapes
+      out[v] = esc ? swv[v] : ((int32_t)k >= 0 ? k : (0x80000000u | (0u - k)));
+    }
+  } else {
+#pragma unroll
+    for (int v = 0; v < PER; ++v) {  // branch-free: lo(b) per element
+      const U bw = bwv[v];
+      const U bits = bits_of_key64(lo_key<T>((int64_t)(I)bw, h.eps) + (int64_t)swv[v]);
+      out[v] = bw == VT<T>::kSentinel ? swv[v] : bits;
+    }
   }
   T* O = static_cast<T*>(a.out) + e0 + i0;
   if ((uint32_t)i0 + PER <= cnt && ((uintptr_t)O & 15) == 0) {
@@ -1299,6 +1400,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kCodecThreads, 6) k_
   const uint64_t nclu = gridDim.x / 2;
   for (uint64_t l = blockIdx.x / 2; l < ncnk; l += nclu) {
     __syncthreads();  // this CTA's previous reconstruct is done with its smem
+    if (tid == 0) {
+      sm.tmin = INT_MAX;
+      sm.tmax = INT_MIN;
+    }
     const uint32_t sz = a.table[2 * l + r];
     const uint8_t* p = a.base + a.off[l] + (r ? a.table[2 * l] : 0u);
     if (h.dtype == 0)
@@ -1322,9 +1427,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kCodecThreads, 6) k_
       const int half_w = h.dtype == 0 ? 2048 : 1024;  // W / 2
       const uint8_t* own = sm.Wd;
       if (h.dtype == 0)
-        reconstruct_half<float>(a, h, (uint32_t)c, r, r ? sm.O : own, r ? half_w : 0, r ? own : sm.O, 0);
+        reconstruct_half<float>(a, h, (uint32_t)c, r, r ? sm.O : own, r ? half_w : 0, r ? own : sm.O, 0, sm);
       else
-        reconstruct_half<double>(a, h, (uint32_t)c, r, r ? sm.O : own, r ? half_w : 0, r ? own : sm.O, 0);
+        reconstruct_half<double>(a, h, (uint32_t)c, r, r ? sm.O : own, r ? half_w : 0, r ? own : sm.O, 0, sm);
     }
   }
   cl.sync();  // no CTA leaves while its partner may still read its flags

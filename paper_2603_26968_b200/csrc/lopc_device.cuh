@@ -121,6 +121,18 @@ __device__ __forceinline__ int32_t lo_key32(int64_t b, double eps) {
   if ((double)f == p && __fma_rn(a, eps, -p) > 0.0) k += 1;  // p exact in f32 but below a*eps
   return k;
 }
+// lo_key32 without branches, for a regular f32 bin (|b| < 2^31; any b gives
+// some value, so the caller may select it away for escapes).  The key stays
+// in int32: |key(lo(b)) + s| < 2^31 for a regular point (its decoded value is
+// a finite float).
+__device__ __forceinline__ int32_t lo_key32_nb(int32_t b, double eps) {
+  const double a = __dadd_rn(i64_to_f64_exact(b), -0.5);
+  const double p = __dmul_rn(a, eps);
+  const float f = __double2float_ru(p);
+  const uint32_t u = __float_as_uint(f);
+  const int32_t k = (int32_t)u >= 0 ? (int32_t)u : -(int32_t)(u & 0x7fffffffu);
+  return k + (int32_t)(((double)f == p) & (__fma_rn(a, eps, -p) > 0.0));
+}
 __device__ __forceinline__ int64_t lo_key64(int64_t b, double eps) {
   const double a = i64_to_f64_exact(b) - 0.5;
   const double p = __dmul_rn(a, eps);
