@@ -434,16 +434,35 @@ __global__ void __launch_bounds__(kRepairThreads, 3) k_quant_flags(RepairArgs a,
                    : "=r"(done)
                    : "r"(sb)
                    : "memory");
-    const U* raw = reinterpret_cast<const U*>(qf_smem);
-    for (int i = tid; i < NB; i += kRepairThreads) {
-      const U u = raw[i];
-      bool ok = (u & ~VT<T>::kSignBit) <= VT<T>::kInfBits;  // not NaN
+    // raw bits -> keys in place, 16 bytes per step (EV elements); a row of
+    // the box is HXS / EV vectors, so the row test is once per vector
+    // (the plain-load instantiation never takes this path: EV = 1 there)
+    constexpr int EV = HXS % (16 / (int)sizeof(U)) == 0 ? 16 / (int)sizeof(U) : 1, VPR = HXS / EV;
+    struct alignas(EV * sizeof(U)) Vec {
+      U e[EV];
+    };
+    Vec* v4 = reinterpret_cast<Vec*>(qf_smem);
+    for (int i4 = tid; i4 < NB / EV; i4 += kRepairThreads) {
+      Vec v = v4[i4];
+      U* u = v.e;
+      bool rowok = true;
+      int hx0 = 0;
       if (!interior) {
-        const int hz = i / (G::HY * HXS), hy = (i / HXS) % G::HY, hx = i % HXS;
-        const Idx gz = z0 + hz - G::ZH, gy = y0 + hy - 1, gx = x0 + hx - 1 - XO;
-        ok = ok && gz >= 0 && gz < d0 && gy >= 0 && gy < d1 && gx >= 0 && gx < d2;
+        const int row = i4 / VPR, hz = row / G::HY, hy = row % G::HY;
+        hx0 = (i4 % VPR) * EV;
+        const Idx gz = z0 + hz - G::ZH, gy = y0 + hy - 1;
+        rowok = gz >= 0 && gz < d0 && gy >= 0 && gy < d1;
       }
-      K[i] = ok ? (I)key_of(u) : kLow;
+#pragma unroll
+      for (int e = 0; e < EV; ++e) {
+        bool ok = (u[e] & ~VT<T>::kSignBit) <= VT<T>::kInfBits;  // not NaN
+        if (!interior) {
+          const Idx gx = x0 + (hx0 + e) - 1 - XO;
+          ok = ok && rowok && gx >= 0 && gx < d2;
+        }
+        u[e] = (U)(ok ? (I)key_of(u[e]) : kLow);
+      }
+      v4[i4] = v;
     }
   } else {
     // halo: keys only
@@ -488,10 +507,15 @@ __global__ void __launch_bounds__(kRepairThreads, 3) k_quant_flags(RepairArgs a,
     uint32_t wv[G::SW];  // the ballots are warp-uniform: lane 0 stores the segment
 #pragma unroll
     for (int j = 0; j < G::SW; ++j) wv[j] = 0;
+    // lok <= kn < kp (+e) / <= kp (-e) as one unsigned range test per slot:
+    // (kn - lok) mod 2^w < span; span = 0 for an escaped / NaN p (no arcs)
+    using UI = typename std::make_unsigned<I>::type;
+    const UI span = lok <= kp ? (UI)((UI)kp - (UI)lok) : (UI)0;
+    const UI spanle = lok <= kp ? (UI)(span + 1u) : (UI)0;
 #pragma unroll
     for (int j = 0; j < 2 * D; ++j) {
       const I kn = K[h + slot_dz<NDIM>(j) * G::HY * HXS + slot_dy<NDIM>(j) * HXS + slot_dx<NDIM>(j)];
-      const bool arc = kn >= lok && (j < D ? kn < kp : kn <= kp);
+      const bool arc = (UI)((UI)kn - (UI)lok) < (j < D ? span : spanle);
       wv[j] = __ballot_sync(0xffffffffu, arc);
     }
     const Idx gz = z0 + lz, gy = y0 + ly;

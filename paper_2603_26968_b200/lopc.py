@@ -87,8 +87,46 @@ def load(require_gpu: bool = True):
     return _lib
 
 
+_dims_cache: dict = {}
+
+
 def _dims(shape):
-    return (C.c_uint64 * 3)(*([int(v) for v in shape] + [0] * (3 - len(shape))))
+    key = tuple(int(v) for v in shape)
+    d = _dims_cache.get(key)
+    if d is None:
+        d = (C.c_uint64 * 3)(*(list(key) + [0] * (3 - len(key))))
+        _dims_cache[key] = d
+    return d
+
+
+class _on_device:
+    """torch.cuda.device(dev) only when dev is not already current (the
+    context switch costs host time on every call)."""
+
+    __slots__ = ("ctx",)
+
+    def __init__(self, dev):
+        self.ctx = torch.cuda.device(dev) if dev.index is not None and dev.index != torch.cuda.current_device() else None
+
+    def __enter__(self):
+        if self.ctx is not None:
+            self.ctx.__enter__()
+
+    def __exit__(self, *a):
+        if self.ctx is not None:
+            self.ctx.__exit__(*a)
+
+
+_size_cache: dict = {}
+
+
+def _cached_size(fn_name: str, *args) -> int:
+    key = (fn_name,) + tuple(int(a) if not isinstance(a, C.Array) else tuple(a) for a in args)
+    v = _size_cache.get(key)
+    if v is None:
+        v = int(getattr(load(False), fn_name)(*args))
+        _size_cache[key] = v
+    return v
 
 
 def _dtype_code(dt) -> int:
@@ -133,14 +171,13 @@ def compress(x: torch.Tensor, eps: float, out: torch.Tensor | None = None) -> to
         raise ValueError("x must be 2D or 3D")
     x = x.contiguous()
     dev = x.device if x.is_cuda else torch.device("cuda", torch.cuda.current_device())
-    cap = compress_bound(x.shape, x.dtype)
     if out is None:
-        out = torch.empty(cap, dtype=torch.uint8, device=x.device)
+        out = torch.empty(compress_bound(x.shape, x.dtype), dtype=torch.uint8, device=x.device)
     host_io = int((not x.is_cuda) or (not out.is_cuda))
-    need = L.lopc_compress_workspace_bytes(x.dim(), _dims(x.shape), _dtype_code(x.dtype), host_io)
+    need = _cached_size("lopc_compress_workspace_bytes", x.dim(), _dims(x.shape), _dtype_code(x.dtype), host_io)
     ws = _workspace(need, dev)
     nbytes = C.c_size_t(out.numel())
-    with torch.cuda.device(dev):
+    with _on_device(dev):
         rc = L.lopc_compress_ex(C.c_void_p(x.data_ptr()), x.dim(), _dims(x.shape), _dtype_code(x.dtype),
                                 float(eps), C.c_void_p(out.data_ptr()), C.byref(nbytes),
                                 C.c_void_p(ws.data_ptr()), ws.numel(), _stream(dev))
@@ -175,9 +212,9 @@ def decompress(stream: torch.Tensor, out: torch.Tensor | None = None, info: dict
                                           torch.device("cuda", torch.cuda.current_device()))
     host_io = int((not stream.is_cuda) or (not out.is_cuda))
     nb = out.numel() * out.element_size()
-    need = L.lopc_decompress_workspace_bytes(stream.numel(), nb, host_io)
+    need = _cached_size("lopc_decompress_workspace_bytes", stream.numel(), nb, host_io)
     ws = _workspace(need, dev)
-    with torch.cuda.device(dev):
+    with _on_device(dev):
         rc = L.lopc_decompress_ex(C.c_void_p(stream.data_ptr()), stream.numel(), C.c_void_p(out.data_ptr()), nb,
                                   C.c_void_p(ws.data_ptr()), ws.numel(), _stream(dev))
     _check(rc, "lopc_decompress")
