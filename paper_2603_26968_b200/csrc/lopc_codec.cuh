@@ -751,7 +751,7 @@ struct EncSmem {
 };
 
 template <typename T, int ROLE>
-__global__ void __launch_bounds__(kCodecThreads, 6) k_encode(EncodeArgs a) {
+__global__ void __launch_bounds__(kCodecThreads, LOPC_CODEC_CTAS) k_encode(EncodeArgs a) {
   using U = typename VT<T>::U;
   using I = typename VT<T>::I;
   constexpr bool SUBS = ROLE == 2;
@@ -1377,7 +1377,7 @@ __device__ __forceinline__ void cluster_sync_relaxed() {
   asm volatile("barrier.cluster.arrive.relaxed.aligned;\n\tbarrier.cluster.wait.aligned;" ::: "memory");
 }
 
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kCodecThreads, 6) k_decode(DecodeArgs a) {
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kCodecThreads, LOPC_CODEC_CTAS) k_decode(DecodeArgs a) {
   namespace cg = cooperative_groups;
   extern __shared__ __align__(16) uint8_t smem_raw[];
   DecSmem& sm = *reinterpret_cast<DecSmem*>(smem_raw);

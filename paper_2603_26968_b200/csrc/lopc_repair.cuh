@@ -64,6 +64,12 @@ struct Geo<2> {
   static constexpr int SW = 8;  // 6 used
 };
 
+#ifndef LOPC_SWEEP_CTAS
+#define LOPC_SWEEP_CTAS 3  // k_sweep CTAs per SM (register budget 85; 4 and 5 measured slower)
+#endif
+#ifndef LOPC_CODEC_CTAS
+#define LOPC_CODEC_CTAS 6  // k_encode / k_decode CTAs per SM (register budget 40; 4 and 5 measured slower)
+#endif
 constexpr int kRepairThreads = 512;
 constexpr int kSweepThreads = 256;
 constexpr int kSweepWarps = kSweepThreads / 32;
@@ -584,7 +590,7 @@ struct SweepSmem {
 };
 
 template <int NDIM, typename Idx>
-__global__ void __launch_bounds__(kSweepThreads, 3) k_sweep(RepairArgs a) {
+__global__ void __launch_bounds__(kSweepThreads, LOPC_SWEEP_CTAS) k_sweep(RepairArgs a) {
   namespace cg = cooperative_groups;
   using G = Geo<NDIM>;
   using UIdx = typename std::make_unsigned<Idx>::type;

@@ -14,7 +14,7 @@ import re
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-SO = os.path.join(_HERE, "liblopc.so")
+SO = os.environ.get("LOPC_LIB") or os.path.join(_HERE, "liblopc.so")  # LOPC_LIB: variant builds (tools)
 HEADER = os.path.join(os.path.dirname(_HERE), "include", "lopc.h")
 
 F32, F64 = 0, 1

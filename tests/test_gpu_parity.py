@@ -114,6 +114,29 @@ def test_long_chains_cross_many_tiles(ref, gpu):
     check_all(ref, gpu, x2, 10.0)
 
 
+@pytest.mark.parametrize("dt", ["f32", "f64"])
+def test_every_bit_plane_count(ref, gpu, dt):
+    """Chunk c holds decreasing ramps of length 2^c in one bin (subbins up to
+    2^c - 1: exactly c non-zero subbin planes), then a chunk of wide random
+    bins: every plane-count path of the codec — the
+    ballot / broadcast BIT paths (P <= 8 / <= 3), the transposes, the
+    zero-tail RZE in both directions, escapes forcing the general path — must
+    give the oracle's bytes."""
+    k = 4 if dt == "f32" else 8
+    W = 16384 // k
+    npd = np.float32 if dt == "f32" else np.float64
+    chunks = []
+    for c in range(11):  # bin 3c, centred: ramps of 1e-4 steps stay inside it
+        L = 1 << c
+        chunks.append(6.0 * c + 0.5 - 1e-4 * (np.arange(W) % L))
+    chunks.append(np.random.default_rng(1).normal(0, 1e4, W))  # wide bin deltas: all planes
+    x = np.concatenate(chunks).astype(npd).reshape(1, -1)
+    check_all(ref, gpu, x, 2.0)
+    y = x.copy()
+    y.ravel()[[3, W + 7, 5 * W + 1]] = [np.inf, np.nan, -np.inf]  # escapes in three chunks
+    check_all(ref, gpu, y, 2.0)
+
+
 def test_escapes_and_edges(ref, gpu):
     x = random_field((37, 41), "f32", "noise", 8)
     x.ravel()[[0, 5, 99, 1000]] = [np.nan, np.inf, -np.inf, 3e38]
