@@ -9,8 +9,13 @@
 // written once, at its final place.  Stream format: DESIGN.md §4.
 //
 // Word buffers in shared memory use an XOR swizzle so that the 32x32 bit
-// transposes of BIT_k run bank-conflict-free: word w lives at
-//   (w & ~31) | ((w ^ (w >> 5)) & 31).
+// transposes of BIT_k run bank-conflict-free.  u32 words (f32): the 16-byte
+// chunk index within a 32-word group is XORed with the group's low 3 bits,
+//   w ^ (((w >> 5) & 7) << 2),
+// so 4-word aligned runs stay contiguous and in order (every access of 4+
+// consecutive words is one 128-bit LDS/STS) and a quarter-warp reading the
+// same chunk of 8 consecutive groups hits 8 distinct bank quads.  u64 words
+// (f64): word w lives at (w & ~31) | ((w ^ (w >> 5)) & 31) (scalar accesses).
 #pragma once
 #include "lopc_device.cuh"
 #include "lopc_repair.cuh"
@@ -19,7 +24,13 @@ namespace lopc {
 
 constexpr int kCodecThreads = 256;
 
-__device__ __forceinline__ int swz(int w) { return (w & ~31) | ((w ^ (w >> 5)) & 31); }
+template <typename U>
+__device__ __forceinline__ int swz(int w) {
+  if constexpr (sizeof(U) == 4)
+    return w ^ (((w >> 5) & 7) << 2);
+  else
+    return (w & ~31) | ((w ^ (w >> 5)) & 31);
+}
 
 // ---------------------------------------------------------------------------
 // Block-wide exclusive scan (sum) over NT threads.
@@ -526,17 +537,37 @@ __device__ __forceinline__ int bit_forward_inplace(uint8_t* buf, int W, unsigned
   uint32_t A[32];
   uint32_t orv = 0;
   if (t < items) {
-    U prev = (DIFF && g) ? words[swz(32 * g - 1)] : (U)0;
+    if constexpr (sizeof(U) == 4) {  // 8 conflict-free 128-bit loads (swz<u32>)
+      const uint4* w4 = reinterpret_cast<const uint4*>(buf);
 #pragma unroll
-    for (int i = 0; i < 32; ++i) {
-      U w = words[swz(32 * g + i)];
-      if (DIFF) {
-        const U cur = w;
-        w = (U)(((U)(cur - prev) + nb_mask<U>()) ^ nb_mask<U>());
-        prev = cur;
+      for (int j = 0; j < 8; ++j) {
+        const uint4 v = w4[8 * g + (j ^ (g & 7))];
+        A[4 * j] = v.x, A[4 * j + 1] = v.y, A[4 * j + 2] = v.z, A[4 * j + 3] = v.w;
       }
-      A[i] = (uint32_t)(w >> (32 * half));
-      orv |= A[i];
+      if (DIFF) {
+        U prev = g ? words[swz<U>(32 * g - 1)] : (U)0;
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          const U cur = A[i];
+          A[i] = (uint32_t)(((U)(cur - prev) + nb_mask<U>()) ^ nb_mask<U>());
+          prev = cur;
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < 32; ++i) orv |= A[i];
+    } else {
+      U prev = (DIFF && g) ? words[swz<U>(32 * g - 1)] : (U)0;
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        U w = words[swz<U>(32 * g + i)];
+        if (DIFF) {
+          const U cur = w;
+          w = (U)(((U)(cur - prev) + nb_mask<U>()) ^ nb_mask<U>());
+          prev = cur;
+        }
+        A[i] = (uint32_t)(w >> (32 * half));
+        orv |= A[i];
+      }
     }
     transpose32(A);
   }
@@ -574,7 +605,7 @@ __device__ __forceinline__ void bit_forward_ballot_p(uint8_t* buf, int W) {
 #pragma unroll
   for (int k = 0; k < 16; ++k) {
     if (k < gpw) {
-      const uint32_t w = (uint32_t)words[swz(32 * (gpw * warp + k) + lane)];
+      const uint32_t w = (uint32_t)words[swz<U>(32 * (gpw * warp + k) + lane)];
 #pragma unroll
       for (int j = 0; j < P; ++j) {
         const uint32_t v = __ballot_sync(0xffffffffu, (w & (1u << j)) != 0u);
@@ -621,9 +652,15 @@ __device__ __forceinline__ void bit_inverse_inplace(uint8_t* buf, int W, int P) 
   }
   __syncthreads();
   if (t < items) {
-    uint32_t* w32 = reinterpret_cast<uint32_t*>(buf);
+    if constexpr (sizeof(U) == 4) {  // 8 conflict-free 128-bit stores (swz<u32>)
+      uint4* w4 = reinterpret_cast<uint4*>(buf);
 #pragma unroll
-    for (int i = 0; i < 32; ++i) w32[swz(32 * g + i) * (int)(sizeof(U) / 4) + half] = A[i];
+      for (int j = 0; j < 8; ++j) w4[8 * g + (j ^ (g & 7))] = make_uint4(A[4 * j], A[4 * j + 1], A[4 * j + 2], A[4 * j + 3]);
+    } else {
+      uint32_t* w32 = reinterpret_cast<uint32_t*>(buf);
+#pragma unroll
+      for (int i = 0; i < 32; ++i) w32[swz<U>(32 * g + i) * 2 + half] = A[i];
+    }
   }
   __syncthreads();
 }
@@ -651,7 +688,7 @@ __device__ __forceinline__ void bit_inverse_small_p(uint8_t* buf, int W) {
   U* words = reinterpret_cast<U*>(buf);
 #pragma unroll
   for (int k = 0; k < 16; ++k)
-    if (k < gpw) words[swz(32 * (gpw * warp + k) + lane)] = (U)wv[k];
+    if (k < gpw) words[swz<U>(32 * (gpw * warp + k) + lane)] = (U)wv[k];
   __syncthreads();
 }
 
@@ -856,8 +893,13 @@ __global__ void __launch_bounds__(kCodecThreads, LOPC_CODEC_CTAS) k_encode(Encod
           orw |= wv[q];
         }
       }
+      const int i4 = 4 * ((hh * (NV / 4) + v) * kCodecThreads + tid);
+      if constexpr (sizeof(U) == 4) {
+        *reinterpret_cast<uint4*>(&WD[swz<U>(i4)]) = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+      } else {
 #pragma unroll
-      for (int q = 0; q < 4; ++q) WD[swz(4 * ((hh * (NV / 4) + v) * kCodecThreads + tid) + q)] = wv[q];
+        for (int q = 0; q < 4; ++q) WD[swz<U>(i4 + q)] = wv[q];
+      }
     }
   }
   if constexpr (SUBS) {  // a4 queue: one warp scan per thread-mask; OR of the words
@@ -895,7 +937,7 @@ __global__ void __launch_bounds__(kCodecThreads, LOPC_CODEC_CTAS) k_encode(Encod
       const T x = X[i];
       I b = 0;
       if (!qtry(x, a.inv32, a.inv, b)) b = (I)quantize_slow<T>(x, a.eps, a.inv);
-      const uint32_t sq = (uint32_t)WD[swz(i)];
+      const uint32_t sq = (uint32_t)WD[swz<U>(i)];
       if ((int64_t)lo_key<T>((int64_t)b, a.eps) + (int64_t)sq > (int64_t)key_of((U)as_bits(x))) bad = 1;
     }
     if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(&a.ctr->err, kErrBound);
@@ -1216,7 +1258,7 @@ __device__ __noinline__ void decode_stream(const DecodeArgs& a, const uint8_t* p
   pc.start(a.prof);
   if (size == kChunkBytes) {  // raw words
     const U* g = reinterpret_cast<const U*>(p);
-    for (int i = tid; i < W; i += kCodecThreads) WD[swz(i)] = g[i];
+    for (int i = tid; i < W; i += kCodecThreads) WD[swz<U>(i)] = g[i];
     __syncthreads();
     pc.mark(a.ctr, subs ? 10 : 9);
     return;
@@ -1259,7 +1301,16 @@ __device__ __noinline__ void decode_stream(const DecodeArgs& a, const uint8_t* p
     U run = 0;
 #pragma unroll
     for (int v = 0; v < PER; ++v) {
-      const U u = WD[swz(tid * PER + v)];
+      U u;
+      if constexpr (sizeof(U) == 4) {
+        if (v % 4 == 0) {
+          const uint4 q = *reinterpret_cast<const uint4*>(&WD[swz<U>(tid * PER + v)]);
+          d[v] = q.x, d[v + 1] = q.y, d[v + 2] = q.z, d[v + 3] = q.w;
+        }
+        u = d[v];
+      } else {
+        u = WD[swz<U>(tid * PER + v)];
+      }
       d[v] = (U)((u ^ nb_mask<U>()) - nb_mask<U>());
       run += d[v];
     }
@@ -1273,7 +1324,16 @@ __device__ __noinline__ void decode_stream(const DecodeArgs& a, const uint8_t* p
 #pragma unroll
     for (int v = 0; v < PER; ++v) {
       acc += d[v];
-      WD[swz(tid * PER + v)] = acc;
+      d[v] = acc;
+    }
+#pragma unroll
+    for (int v = 0; v < PER; ++v) {
+      if constexpr (sizeof(U) == 4) {
+        if (v % 4 == 0)
+          *reinterpret_cast<uint4*>(&WD[swz<U>(tid * PER + v)]) = make_uint4(d[v], d[v + 1], d[v + 2], d[v + 3]);
+      } else {
+        WD[swz<U>(tid * PER + v)] = d[v];
+      }
     }
     __syncthreads();
     pc.mark(a.ctr, 12);
@@ -1300,8 +1360,17 @@ __device__ __forceinline__ void reconstruct_half(const DecodeArgs& a, const Hdr&
   U bwv[PER], swv[PER];
 #pragma unroll
   for (int v = 0; v < PER; ++v) {
-    bwv[v] = WB[swz(i0 + v - wb_off)];
-    swv[v] = SW[swz(i0 + v - ws_off)];
+    if constexpr (sizeof(U) == 4) {  // 4-word runs are contiguous (swz<u32>)
+      if (v % 4 == 0) {
+        const uint4 b = *reinterpret_cast<const uint4*>(&WB[swz<U>(i0 + v - wb_off)]);
+        const uint4 q = *reinterpret_cast<const uint4*>(&SW[swz<U>(i0 + v - ws_off)]);
+        bwv[v] = b.x, bwv[v + 1] = b.y, bwv[v + 2] = b.z, bwv[v + 3] = b.w;
+        swv[v] = q.x, swv[v + 1] = q.y, swv[v + 2] = q.z, swv[v + 3] = q.w;
+      }
+    } else {
+      bwv[v] = WB[swz<U>(i0 + v - wb_off)];
+      swv[v] = SW[swz<U>(i0 + v - ws_off)];
+    }
   }
   U out[PER];
   if constexpr (sizeof(U) == 4) {
