@@ -76,9 +76,18 @@ constexpr int kSweepWarps = kSweepThreads / 32;
 constexpr int kPassHist = 16;
 constexpr int kLevelPlanes = 8;  // dense-pass levels per tile before handing over to the worklist
 constexpr unsigned long long kSmallList = 256;
-constexpr int kChase = 8;          // depth-first successor stack per lane in the sparse passes
-constexpr int kChaseBudget = 12;   // chased evaluations per list point
-constexpr unsigned long long kChaseMaxList = 1ull << 18;  // chase only when the pass list is at most this long  // sparse passes this short run on one block
+#ifndef LOPC_CHASE
+#define LOPC_CHASE 8
+#endif
+#ifndef LOPC_CHASE_BUDGET
+#define LOPC_CHASE_BUDGET 12
+#endif
+#ifndef LOPC_CHASE_MAX_LOG2
+#define LOPC_CHASE_MAX_LOG2 18
+#endif
+constexpr int kChase = LOPC_CHASE;                // depth-first successor stack per lane in the sparse passes
+constexpr int kChaseBudget = LOPC_CHASE_BUDGET;   // chased evaluations per list point
+constexpr unsigned long long kChaseMaxList = 1ull << LOPC_CHASE_MAX_LOG2;  // chase only when the pass list is at most this long
 constexpr int kMaxLevel = (1 << kLevelPlanes) - 1;
 
 // Star slot j (G2): j < D is +e, j >= D is -e, with e = (j mod D) + 1 read

@@ -1,0 +1,10 @@
+# Full round evidence: the whole GPU test suite, the default bench (with the
+# CPU baselines), the reference arm, and the ncu captures (full set on one
+# cfg2 step + the per-launch duration list of a short bench run).
+TAG=${1:-r1}
+python -c "import __graft_entry__ as g; g.build(); g.smoke()" > gpurun_out/smoke_${TAG}.log 2>&1
+timeout 1800 python -m pytest tests -m gpu -q --timeout 1700 -x --durations=15 > gpurun_out/gpu_tests_${TAG}.log 2>&1
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,clocks_throttle_reasons.active --format=csv > gpurun_out/smi_${TAG}.txt
+timeout 600 python bench.py > gpurun_out/bench_${TAG}.json 2> gpurun_out/bench_${TAG}.err
+timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref_${TAG}.json 2>&1
+bash tools/profile_round.sh ${TAG}
