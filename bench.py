@@ -627,8 +627,8 @@ def main():
                 "note": "lopc_compress/lopc_decompress on pinned host buffers, staging copies inside the call"},
         "gpu_launches": launches_timed,
         "clocks": clk.summary(),
-        "notes": "per_kernel/roofline: the library's per-launch events with launches serialized (lopc_set_timing); "
-                 "the timed region runs the bin-stream encode on a side stream beside the repair",
+        "notes": "per_kernel/roofline: the library's per-launch events (lopc_set_timing) in a second loop; "
+                 "launches run in stream order in both loops",
     }
     print(json.dumps(line), flush=True)
     if dist:

@@ -11,6 +11,7 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 
@@ -582,7 +583,13 @@ int lopc_compress_ex(const void* in, int ndims, const uint64_t* dims, int dtype,
   // The bin stream depends on x only: without per-kernel timing its CTAs run
   // on a side stream beside the (latency-bound) repair; the subbin CTAs follow
   // the repair on the call's stream.  With timing on, everything is serial.
-  const bool overlap = !tm.on;
+  // LOPC_OVERLAP=1 runs the bin-stream encode on a side stream beside the
+  // repair (it only depends on x), =2 before it; measured on cfg2 (r1f) both
+  // are slower than the default serial order (0.665 / 0.656 vs 0.651 ms): the
+  // repair leaves no room on the SMs (k_sweep fills the register file).
+  static const int ovl_mode = getenv("LOPC_OVERLAP") ? atoi(getenv("LOPC_OVERLAP")) : 0;
+  const bool overlap = !tm.on && ovl_mode == 1;
+  if (!tm.on && ovl_mode == 2) launch_encode(ea, sh.dtype == LOPC_F64, 1, (unsigned)sh.C, smem, st);
   if (overlap) {
     CK(cudaEventRecord(di->ev_fork, st));
     CK(cudaStreamWaitEvent(di->side, di->ev_fork, 0));
@@ -591,7 +598,7 @@ int lopc_compress_ex(const void* in, int ndims, const uint64_t* dims, int dtype,
     CK(cudaEventRecord(di->ev_join, di->side));
   }
   if ((rc = run_repair(sh, x, eps, ws, L, st, tm, hc))) return rc;  // marks 3, 4
-  if (!overlap) launch_encode(ea, sh.dtype == LOPC_F64, 1, (unsigned)sh.C, smem, st);
+  if (!overlap && !(!tm.on && ovl_mode == 2)) launch_encode(ea, sh.dtype == LOPC_F64, 1, (unsigned)sh.C, smem, st);
   launch_encode(ea, sh.dtype == LOPC_F64, 2, (unsigned)sh.C, smem, st);
   CK(cudaGetLastError());
   if (overlap) CK(cudaStreamWaitEvent(st, di->ev_join, 0));
