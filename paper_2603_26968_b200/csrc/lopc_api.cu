@@ -580,9 +580,7 @@ int lopc_compress_ex(const void* in, int ndims, const uint64_t* dims, int dtype,
   ea.d2 = sh.d2;
   set_escape_limits(ea, sh.dtype == LOPC_F64, eps);
   const size_t smem = sizeof(EncSmem);
-  // The bin stream depends on x only: without per-kernel timing its CTAs run
-  // on a side stream beside the (latency-bound) repair; the subbin CTAs follow
-  // the repair on the call's stream.  With timing on, everything is serial.
+  // Stream order: repair, bin-stream encode, subbin-stream encode.
   // LOPC_OVERLAP=1 runs the bin-stream encode on a side stream beside the
   // repair (it only depends on x), =2 before it; measured on cfg2 (r1f) both
   // are slower than the default serial order (0.665 / 0.656 vs 0.651 ms): the
