@@ -555,7 +555,7 @@ __device__ __forceinline__ int bit_forward_inplace(uint8_t* buf, int W, unsigned
       }
 #pragma unroll
       for (int i = 0; i < 32; ++i) orv |= A[i];
-    } else {
+    } else {  // (f64: the high-half items usually see all-zero words)
       U prev = (DIFF && g) ? words[swz<U>(32 * g - 1)] : (U)0;
 #pragma unroll
       for (int i = 0; i < 32; ++i) {
@@ -569,7 +569,7 @@ __device__ __forceinline__ int bit_forward_inplace(uint8_t* buf, int W, unsigned
         orv |= A[i];
       }
     }
-    transpose32(A);
+    if (orv) transpose32(A);  // all-zero input: already its own transpose
   }
   // warps lie within one half (groups is a multiple of 32)
   orv = __reduce_or_sync(0xffffffffu, orv);
@@ -648,7 +648,7 @@ __device__ __forceinline__ void bit_inverse_inplace(uint8_t* buf, int W, int P) 
     const uint32_t* planes = reinterpret_cast<const uint32_t*>(buf);
 #pragma unroll
     for (int j = 0; j < 32; ++j) A[j] = 32 * half + j < P ? planes[(32 * half + j) * groups + g] : 0u;
-    transpose32(A);
+    if (32 * half < P) transpose32(A);  // planes of this half all zero (f64 high half): zeros
   }
   __syncthreads();
   if (t < items) {
