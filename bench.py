@@ -594,6 +594,22 @@ def main():
     if os.path.exists(tp):
         traffic = json.load(open(tp)).get(f"k_{dom}")
 
+    # the bound these kernels actually hit: instruction issue.  Peak = 4
+    # schedulers x 1 warp-instruction/clk x 148 SMs x the sampled SM clock
+    # (B200_PROFILING.md / blackwell guide unit counts); instructions per
+    # launch from the committed ncu capture of the same kernel and config.
+    issue = None
+    wp = os.path.join(ROOT, "profiles", f"warpinst_{args.config}.json")
+    if os.path.exists(wp) and med[dom] > 0:
+        wi = json.load(open(wp))["kernels"].get(f"k_{dom}")
+        if wi:
+            mhz = clk.summary().get("sm_mhz") or 1965.0
+            ipk = 4 * 148 * mhz * 1e6
+            ach = wi / (med[dom] / 1e3)
+            issue = {"kernel": f"k_{dom}", "bound": "issue", "achieved": ach, "peak": ipk,
+                     "unit": "warp-instructions/s", "frac": ach / ipk, "warp_instructions": wi,
+                     "source": os.path.relpath(wp, ROOT)}
+
     cpu = cpu_omp = None
     if not args.no_cpu_baseline:
         xs_host = x_np if x_np is not None else x[:1].cpu().numpy()  # cfg5: the leading plane
@@ -620,6 +636,7 @@ def main():
         "roofline": {"kernel": f"k_{dom}", "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                      "alg_bytes_per_launch": alg[dom], "launch_ms": med[dom]},
+        "roofline_issue": issue,
         "cpu_baseline": cpu,
         "cpu_baseline_multicore": cpu_omp,
         "e2e": {"value": e2e_val, "unit": "GB/s", "h2d_bytes_per_step": raw + nbytes_stream,

@@ -10,6 +10,8 @@ gpu__time_duration launch list of `bench.py --steps 2 --warmup 1`), writes
   profiles/TAG_launches.csv       the launch list (our kernels only)
   profiles/traffic_CONFIG.json    dram read+write bytes per launch (bench.py's
                                   roofline.traffic)
+  profiles/warpinst_CONFIG.json   warp instructions per launch (bench.py's
+                                  issue roofline)
 """
 import csv
 import io
@@ -88,6 +90,12 @@ for k, v in out.items():
     name = k[:-2] if k.endswith("_2") and k.startswith("k_encode") else k  # the two encode roles: one step's encode
     traffic[name] = traffic.get(name, 0) + (v["dram_read_bytes"] or 0) + (v["dram_write_bytes"] or 0)
 json.dump(traffic, open(os.path.join(prof, f"traffic_{config}.json"), "w"), indent=1)
+winst = {}
+for k, v in out.items():
+    name = k[:-2] if k.endswith("_2") and k.startswith("k_encode") else k
+    winst[name] = winst.get(name, 0) + (v["warp_instructions"] or 0)
+json.dump({"source": f"{tag}_ncu_summary.json smsp__inst_executed.sum per launch", "kernels": winst},
+          open(os.path.join(prof, f"warpinst_{config}.json"), "w"), indent=1)
 
 # launch list: our kernels only, plus each kernel's share of the step
 lp = os.path.join(ROOT, "gpurun_out", f"launches_{tag}.csv")
