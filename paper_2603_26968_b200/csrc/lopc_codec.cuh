@@ -569,7 +569,7 @@ __device__ __forceinline__ int bit_forward_inplace(uint8_t* buf, int W, unsigned
         orv |= A[i];
       }
     }
-    if (orv) transpose32(A);  // all-zero input: already its own transpose
+    if (sizeof(U) == 4 || orv) transpose32(A);  // f64: all-zero high halves are their own transpose
   }
   // warps lie within one half (groups is a multiple of 32)
   orv = __reduce_or_sync(0xffffffffu, orv);
@@ -648,7 +648,7 @@ __device__ __forceinline__ void bit_inverse_inplace(uint8_t* buf, int W, int P) 
     const uint32_t* planes = reinterpret_cast<const uint32_t*>(buf);
 #pragma unroll
     for (int j = 0; j < 32; ++j) A[j] = 32 * half + j < P ? planes[(32 * half + j) * groups + g] : 0u;
-    if (32 * half < P) transpose32(A);  // planes of this half all zero (f64 high half): zeros
+    if (sizeof(U) == 4 || 32 * half < P) transpose32(A);  // f64 high half with no planes: zeros
   }
   __syncthreads();
   if (t < items) {
