@@ -75,7 +75,10 @@ constexpr int kSweepThreads = 256;
 constexpr int kSweepWarps = kSweepThreads / 32;
 constexpr int kPassHist = 16;
 constexpr int kLevelPlanes = 8;  // dense-pass levels per tile before handing over to the worklist
-constexpr unsigned long long kSmallList = 256;
+#ifndef LOPC_SMALL_LIST
+#define LOPC_SMALL_LIST 256
+#endif
+constexpr unsigned long long kSmallList = LOPC_SMALL_LIST;  // sparse passes this short run on block 0 alone
 #ifndef LOPC_CHASE
 #define LOPC_CHASE 8
 #endif
