@@ -637,27 +637,30 @@ __device__ __forceinline__ void bit_forward_ballot(uint8_t* buf, int W, int P) {
   }
 }
 
-// Inverse BIT_k in place (planes linear -> words swizzled); planes >= P are
-// zero and not read.  All threads must call.
-template <typename U>
-__device__ __forceinline__ void bit_inverse_inplace(uint8_t* buf, int W, int P) {
+// Inverse BIT_k: planes (linear, `pb`) -> words (swizzled, `wb`); planes >= P
+// are zero and not read.  INPLACE (pb == wb): all loads, barrier, all
+// stores; out of place there is no barrier between them, so the 32 staged
+// words are not live across one.
+// All threads must call.
+template <typename U, bool INPLACE>
+__device__ __forceinline__ void bit_inverse_inplace(const uint8_t* pb, uint8_t* wb, int W, int P) {
   const int groups = W / 32, items = groups * (int)(sizeof(U) / 4);
   const int t = threadIdx.x, g = t % groups, half = t / groups;
   uint32_t A[32];
   if (t < items) {
-    const uint32_t* planes = reinterpret_cast<const uint32_t*>(buf);
+    const uint32_t* planes = reinterpret_cast<const uint32_t*>(pb);
 #pragma unroll
     for (int j = 0; j < 32; ++j) A[j] = 32 * half + j < P ? planes[(32 * half + j) * groups + g] : 0u;
     if (sizeof(U) == 4 || 32 * half < P) transpose32(A);  // f64 high half with no planes: zeros
   }
-  __syncthreads();
+  if (INPLACE) __syncthreads();
   if (t < items) {
     if constexpr (sizeof(U) == 4) {  // 8 conflict-free 128-bit stores (swz<u32>)
-      uint4* w4 = reinterpret_cast<uint4*>(buf);
+      uint4* w4 = reinterpret_cast<uint4*>(wb);
 #pragma unroll
       for (int j = 0; j < 8; ++j) w4[8 * g + (j ^ (g & 7))] = make_uint4(A[4 * j], A[4 * j + 1], A[4 * j + 2], A[4 * j + 3]);
     } else {
-      uint32_t* w32 = reinterpret_cast<uint32_t*>(buf);
+      uint32_t* w32 = reinterpret_cast<uint32_t*>(wb);
 #pragma unroll
       for (int i = 0; i < 32; ++i) w32[swz<U>(32 * g + i) * 2 + half] = A[i];
     }
@@ -668,12 +671,12 @@ __device__ __forceinline__ void bit_inverse_inplace(uint8_t* buf, int W, int P) 
 // The same for P <= 3 (the usual subbin chunk) without transposes: lane l of
 // warp w builds word 32 g + l of its groups g from bit l of the P plane words
 // (broadcast loads).  All threads must call.
-template <typename U, int P>
-__device__ __forceinline__ void bit_inverse_small_p(uint8_t* buf, int W) {
+template <typename U, int P, bool INPLACE>
+__device__ __forceinline__ void bit_inverse_small_p(const uint8_t* pb, uint8_t* wb, int W) {
   constexpr int NW = kCodecThreads / 32;
   const int groups = W / 32, gpw = groups / NW;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const uint32_t* planes = reinterpret_cast<const uint32_t*>(buf);
+  const uint32_t* planes = reinterpret_cast<const uint32_t*>(pb);
   uint32_t wv[16];
 #pragma unroll
   for (int k = 0; k < 16; ++k) {
@@ -684,22 +687,22 @@ __device__ __forceinline__ void bit_inverse_small_p(uint8_t* buf, int W) {
       for (int j = 0; j < P; ++j) wv[k] |= ((planes[j * groups + g] >> lane) << j) & (1u << j);
     }
   }
-  __syncthreads();
-  U* words = reinterpret_cast<U*>(buf);
+  if (INPLACE) __syncthreads();
+  U* words = reinterpret_cast<U*>(wb);
 #pragma unroll
   for (int k = 0; k < 16; ++k)
     if (k < gpw) words[swz<U>(32 * (gpw * warp + k) + lane)] = (U)wv[k];
   __syncthreads();
 }
 
-template <typename U>
-__device__ __forceinline__ void bit_inverse_planes(uint8_t* buf, int W, int P) {
+template <typename U, bool INPLACE>
+__device__ __forceinline__ void bit_inverse_planes(const uint8_t* pb, uint8_t* wb, int W, int P) {
   switch (P) {
-    case 0: bit_inverse_small_p<U, 0>(buf, W); break;
-    case 1: bit_inverse_small_p<U, 1>(buf, W); break;
-    case 2: bit_inverse_small_p<U, 2>(buf, W); break;
-    case 3: bit_inverse_small_p<U, 3>(buf, W); break;
-    default: bit_inverse_inplace<U>(buf, W, P); break;
+    case 0: bit_inverse_small_p<U, 0, INPLACE>(pb, wb, W); break;
+    case 1: bit_inverse_small_p<U, 1, INPLACE>(pb, wb, W); break;
+    case 2: bit_inverse_small_p<U, 2, INPLACE>(pb, wb, W); break;
+    case 3: bit_inverse_small_p<U, 3, INPLACE>(pb, wb, W); break;
+    default: bit_inverse_inplace<U, INPLACE>(pb, wb, W, P); break;
   }
 }
 
@@ -1251,7 +1254,9 @@ __device__ __noinline__ void decode_stream(const DecodeArgs& a, const uint8_t* p
   constexpr int K = VT<T>::K;
   constexpr int W = kChunkBytes / K;
   constexpr int PER = W / kCodecThreads;
-  U* WD = reinterpret_cast<U*>(sm.Wd);
+  // words: subbins in place in sm.Wd; bins out of place into sm.O (their
+  // payload there is dead once RZE^-1 has produced the planes in sm.Wd)
+  U* WD = reinterpret_cast<U*>(subs ? sm.Wd : sm.O);
   const int tid = threadIdx.x;
   bool bad = false;
   PhaseClock pc;
@@ -1294,7 +1299,10 @@ __device__ __noinline__ void decode_stream(const DecodeArgs& a, const uint8_t* p
     __syncthreads();
     return;
   }
-  bit_inverse_planes<U>(sm.Wd, W, (int)(act / PB));
+  if (subs)
+    bit_inverse_planes<U, true>(sm.Wd, sm.Wd, W, (int)(act / PB));
+  else
+    bit_inverse_planes<U, false>(sm.Wd, sm.O, W, (int)(act / PB));
   pc.mark(a.ctr, 11);
   if (!subs) {  // NB^-1 + prefix sum (thread owns PER consecutive words)
     U d[PER];
@@ -1347,7 +1355,8 @@ __device__ __noinline__ void decode_stream(const DecodeArgs& a, const uint8_t* p
 // repetitive), and the values leave as 16-byte stores.
 template <typename T>
 __device__ __forceinline__ void reconstruct_half(const DecodeArgs& a, const Hdr& h, uint32_t c, int r, const uint8_t* wb,
-                                                 int wb_off, const uint8_t* ws, int ws_off, DecSmem& sm) {
+                                                 int wb_off, const uint8_t* ws, int ws_off, DecSmem& sm,
+                                                 int32_t* tab) {
   using U = typename VT<T>::U;
   using I = typename VT<T>::I;
   constexpr int W = kChunkBytes / VT<T>::K;
@@ -1377,7 +1386,7 @@ __device__ __forceinline__ void reconstruct_half(const DecodeArgs& a, const Hdr&
     // f32: key(lo(b)) for every bin of the half in a shared table when the
     // half's bin range is small (the usual case: bins are locally smooth),
     // else per element; the same lo_key32_nb either way
-    constexpr int kTab = 2048;  // entries at sm.O + 8 KiB (the partner's half copy is below)
+    constexpr int kTab = 2048;  // entries at `tab` (8 KiB after the copied half)
     int lmin = INT_MAX, lmax = INT_MIN;
 #pragma unroll
     for (int v = 0; v < PER; ++v)
@@ -1394,7 +1403,6 @@ __device__ __forceinline__ void reconstruct_half(const DecodeArgs& a, const Hdr&
     __syncthreads();
     const int tmin = sm.tmin;
     const int64_t R = (int64_t)sm.tmax - (int64_t)tmin + 1;
-    int32_t* tab = reinterpret_cast<int32_t*>(sm.O + kChunkBytes / 2);
     const bool use_tab = R > 0 && R <= kTab;
     if (use_tab) {
       for (int k = threadIdx.x; k < (int)R; k += kCodecThreads) tab[k] = lo_key32_nb(tmin + k, h.eps);
@@ -1483,22 +1491,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kCodecThreads, LOPC_
     const uint64_t c = a.c_begin + l;
     const bool ok = !s0->bad && !s1->bad;
     // the partner's words of this CTA's half, copied once into local smem
-    // with 16-byte DSMEM loads (sm.O is free here)
+    // with 16-byte DSMEM loads: rank 0 (bin words in its sm.O) takes the
+    // subbin half 0 into its sm.Wd (planes, dead); rank 1 (subbin words in its
+    // sm.Wd) takes the bin half 1 into its sm.O (RZE_1 output, dead)
     constexpr int HB = kChunkBytes / 2;
     if (ok) {
-      const uint4* rem = reinterpret_cast<const uint4*>((r ? s0->Wd : s1->Wd) + r * HB);
-      uint4* loc = reinterpret_cast<uint4*>(sm.O);
+      const uint4* rem = reinterpret_cast<const uint4*>(r ? s0->O + HB : s1->Wd);
+      uint4* loc = reinterpret_cast<uint4*>(r ? sm.O : sm.Wd);
       for (int t = tid; t < HB / 16; t += kCodecThreads) loc[t] = rem[t];
     }
     cluster_sync_relaxed();  // both copies done: the partner may overwrite its words next
     __syncthreads();         // the local copy is visible to the whole CTA
     if (ok) {
       const int half_w = h.dtype == 0 ? 2048 : 1024;  // W / 2
-      const uint8_t* own = sm.Wd;
+      // bins in sm.O (rank 1: the copied half, offset W/2), subbins in sm.Wd;
+      // the f32 lo-key table in the free 8 KiB after this CTA's copied half
+      int32_t* tab = reinterpret_cast<int32_t*>((r ? sm.O : sm.Wd) + HB);
       if (h.dtype == 0)
-        reconstruct_half<float>(a, h, (uint32_t)c, r, r ? sm.O : own, r ? half_w : 0, r ? own : sm.O, 0, sm);
+        reconstruct_half<float>(a, h, (uint32_t)c, r, sm.O, r ? half_w : 0, sm.Wd, 0, sm, tab);
       else
-        reconstruct_half<double>(a, h, (uint32_t)c, r, r ? sm.O : own, r ? half_w : 0, r ? own : sm.O, 0, sm);
+        reconstruct_half<double>(a, h, (uint32_t)c, r, sm.O, r ? half_w : 0, sm.Wd, 0, sm, tab);
     }
   }
   cl.sync();  // no CTA leaves while its partner may still read its flags
