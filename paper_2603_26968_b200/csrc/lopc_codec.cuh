@@ -1121,6 +1121,33 @@ struct PlaceArgs {
   double eps;
 };
 
+// one warp copies n words (4-byte aligned destination): 128-bit loads from
+// the 16-byte aligned staging slot, four of them in flight per lane, words
+// stored one by one (the stream offset is only 4-byte aligned)
+__device__ __forceinline__ void place_words(const uint32_t* src, uint32_t* dst, uint32_t n, int lane) {
+  const uint4* s4 = reinterpret_cast<const uint4*>(src);
+  const uint32_t n4 = n / 4;
+  for (uint32_t b = 0; b < n4; b += 128) {
+    uint4 v[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint32_t i = b + 32 * k + lane;
+      v[k] = i < n4 ? __ldcs(&s4[i]) : make_uint4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint32_t i = b + 32 * k + lane;
+      if (i < n4) {
+        dst[4 * i] = v[k].x;
+        dst[4 * i + 1] = v[k].y;
+        dst[4 * i + 2] = v[k].z;
+        dst[4 * i + 3] = v[k].w;
+      }
+    }
+  }
+  for (uint32_t i = 4 * n4 + lane; i < n; i += 32) dst[i] = __ldcs(&src[i]);
+}
+
 __global__ void __launch_bounds__(256) k_place(PlaceArgs a) {
   const int lane = threadIdx.x & 31;
   const uint64_t total = a.ctr->total_bytes;
@@ -1133,8 +1160,8 @@ __global__ void __launch_bounds__(256) k_place(PlaceArgs a) {
     const uint32_t bs = a.sizes[2 * c], ss = a.sizes[2 * c + 1];
     const uint32_t* src = reinterpret_cast<const uint32_t*>(a.stage + (size_t)c * 2 * kChunkBytes);
     uint32_t* dst = reinterpret_cast<uint32_t*>(a.out + a.off[c]);
-    for (uint32_t i = lane; i < bs / 4; i += 32) dst[i] = __ldcs(&src[i]);
-    for (uint32_t i = lane; i < ss / 4; i += 32) dst[bs / 4 + i] = __ldcs(&src[kChunkBytes / 4 + i]);
+    place_words(src, dst, bs / 4, lane);
+    place_words(src + kChunkBytes / 4, dst + bs / 4, ss / 4, lane);
     if (lane == 0) {
       uint32_t* tab = reinterpret_cast<uint32_t*>(a.table + 8ull * c);
       tab[0] = bs;
