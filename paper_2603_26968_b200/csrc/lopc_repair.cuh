@@ -85,6 +85,9 @@ constexpr unsigned long long kSmallList = LOPC_SMALL_LIST;  // sparse passes thi
 #ifndef LOPC_CHASE_BUDGET
 #define LOPC_CHASE_BUDGET 12
 #endif
+#ifndef LOPC_CHASE_MAX_PASS
+#define LOPC_CHASE_MAX_PASS 2  // chase only in the first sparse pass (cfg3 sweep 5.26 -> 4.99 ms, cfg2 unchanged)
+#endif
 #ifndef LOPC_CHASE_MAX_LOG2
 #define LOPC_CHASE_MAX_LOG2 18
 #endif
@@ -884,7 +887,10 @@ __global__ void __launch_bounds__(kSweepThreads, LOPC_SWEEP_CTAS) k_sweep(Repair
       }
       Idx stk[kChase];
       int sp = 0;
-      int budget = n <= kChaseMaxList ? kChaseBudget : 0;  // long lists: plain passes (no redundant chases)
+      // long lists: plain passes (no redundant chases); chasing only in the
+      // early sparse passes (late passes of long-chain fields chase into
+      // each other's work)
+      int budget = (n <= kChaseMaxList && q <= LOPC_CHASE_MAX_PASS) ? kChaseBudget : 0;
       while (__any_sync(0xffffffffu, have)) {
         Idx z = 0, y = 0, x = 0;
         uint32_t best = 0;
