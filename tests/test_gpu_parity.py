@@ -178,6 +178,28 @@ def test_host_buffers_same_bytes(ref, gpu):
     assert y.numpy().tobytes() == ref.decompress(st.numpy().tobytes()).tobytes()
 
 
+def test_output_capacity(ref, gpu):
+    """E_NOSPACE: an output buffer smaller than the stream is
+    refused; a buffer of exactly the stream's size works and gives the
+    oracle's bytes; a decode target smaller than the field is refused."""
+    import torch
+
+    x = random_field((40, 300), "f32", "smooth", 5)
+    eps = eps_noa(x, 1e-3)
+    st_ref = ref.compress(x, eps)
+    xt = _t(x)
+    small = torch.empty(len(st_ref) - 4, dtype=torch.uint8, device="cuda")
+    with pytest.raises(gpu.LopcError) as e:
+        gpu.compress(xt, eps, out=small)
+    assert e.value.code == -3
+    exact = torch.empty(len(st_ref), dtype=torch.uint8, device="cuda")
+    assert gpu.compress(xt, eps, out=exact).cpu().numpy().tobytes() == st_ref
+    st = _t(np.frombuffer(st_ref, np.uint8).copy())
+    with pytest.raises(gpu.LopcError) as e:
+        gpu.decompress(st, out=torch.empty((39, 300), dtype=torch.float32, device="cuda"))
+    assert e.value.code == -3
+
+
 def test_corrupt_streams(ref, gpu):
     import torch
 
