@@ -1024,8 +1024,14 @@ inline void launch_encode(const EncodeArgs& ea, bool f64, int role, unsigned C, 
 // once, so the look-back never waits long).  In decode mode the sizes come
 // from the stream's table and are validated.
 // ---------------------------------------------------------------------------
-constexpr int kScanThreads = 512;
-constexpr int kScanPer = 4;
+#ifndef LOPC_SCAN_THREADS
+#define LOPC_SCAN_THREADS 512
+#endif
+#ifndef LOPC_SCAN_PER
+#define LOPC_SCAN_PER 4
+#endif
+constexpr int kScanThreads = LOPC_SCAN_THREADS;
+constexpr int kScanPer = LOPC_SCAN_PER;
 constexpr int kScanTile = kScanThreads * kScanPer;
 
 struct ScanArgs {
