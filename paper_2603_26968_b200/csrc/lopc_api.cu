@@ -14,6 +14,7 @@
 #include <cstdlib>
 #include <cstdio>
 #include <cstring>
+#include <vector>
 
 #include "../../include/lopc.h"
 #include "lopc_codec.cuh"
@@ -147,6 +148,8 @@ struct DevInfo {
   int dev = -1, sms = 0;
   cudaStream_t side = nullptr;           // bin-stream encode runs here, beside the repair
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaStream_t side2 = nullptr;            // host-I/O decompress: D2H of decoded ranges
+  cudaEvent_t ev_in[4] = {}, ev_dec[4] = {}, ev_out = nullptr;
   int occ_sweep2 = 0, occ_sweep3 = 0, occ_sweep2w = 0, occ_sweep3w = 0, occ_decode = 0;
   bool attrs = false;
 };
@@ -161,6 +164,12 @@ int dev_info(DevInfo*& out) {
     CK(cudaStreamCreateWithFlags(&g_dev.side, cudaStreamNonBlocking));
     CK(cudaEventCreateWithFlags(&g_dev.ev_fork, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&g_dev.ev_join, cudaEventDisableTiming));
+    CK(cudaStreamCreateWithFlags(&g_dev.side2, cudaStreamNonBlocking));
+    for (int i = 0; i < 4; ++i) {
+      CK(cudaEventCreateWithFlags(&g_dev.ev_in[i], cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&g_dev.ev_dec[i], cudaEventDisableTiming));
+    }
+    CK(cudaEventCreateWithFlags(&g_dev.ev_out, cudaEventDisableTiming));
     CK(cudaDeviceGetAttribute(&g_dev.sms, cudaDevAttrMultiProcessorCount, dev));
     const int smem = (int)sizeof(EncSmem), dsmem = (int)sizeof(DecSmem);
     CK(cudaFuncSetAttribute(k_encode<float, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
@@ -736,6 +745,55 @@ int lopc_repair_ex(const void* in, int ndims, const uint64_t* dims, int dtype, d
   return map_err(hc->err);
 }
 
+// Host side of parse_header (k_decode) plus the size-table checks of
+// k_chunk_scan's validating mode, on a stream in host memory; fills the
+// payload offsets.  false: not a valid stream (the caller takes the device
+// path, which reports the precise error).
+static bool host_stream_plan(const uint8_t* in, size_t in_bytes, size_t out_cap, Hdr& h,
+                             std::vector<uint64_t>& off) {
+  if (in_bytes < kHdrBytes) return false;
+  uint32_t h32[16];
+  uint64_t h64[8];
+  memcpy(h32, in, 64);
+  memcpy(h64, in, 64);
+  if (h32[0] != 0x43504f4cu || (h32[1] & 0xffffu) != 1u) return false;
+  h = Hdr{};
+  h.dtype = (h32[1] >> 16) & 0xff;
+  h.ndims = (h32[1] >> 24) & 0xff;
+  if (h.dtype > 1 || (h.ndims != 2 && h.ndims != 3)) return false;
+  h.d0 = h64[1];
+  h.d1 = h64[2];
+  h.d2 = h64[3];
+  if (h.ndims == 2 && h.d0 != 1) return false;
+  const uint64_t lim = 1ull << 40;
+  if (h.d0 > lim || h.d1 > lim || h.d2 > lim || h.d0 * h.d1 > lim) return false;
+  h.n = h64[5];
+  if (h.d0 * h.d1 * h.d2 != h.n || h.n > lim || h.n == 0) return false;
+  memcpy(&h.eps, in + 32, 8);
+  if (!(h.eps >= 0x1p-900 && h.eps <= 0x1p1000)) return false;
+  if (h32[12] != kChunkBytes) return false;
+  const uint64_t W = kChunkBytes / (h.dtype ? 8u : 4u);
+  h.C = h32[13];
+  if ((uint64_t)h.C != (h.n + W - 1) / W || h64[7] != in_bytes) return false;
+  if ((uint64_t)kHdrBytes + 8ull * h.C > in_bytes || h.n * (h.dtype ? 8u : 4u) > out_cap) return false;
+  const uint8_t* tab = in + kHdrBytes;
+  off.resize(h.C);
+  uint64_t o = kHdrBytes + 8ull * h.C;
+  for (uint32_t c = 0; c < h.C; ++c) {
+    uint32_t bs, ss;
+    memcpy(&bs, tab + 8ull * c, 4);
+    memcpy(&ss, tab + 8ull * c + 4, 4);
+    if (!(bs >= 4 && bs <= kChunkBytes && (bs & 3u) == 0 && ss >= 4 && ss <= kChunkBytes && (ss & 3u) == 0))
+      return false;
+    off[c] = o;
+    o += bs + ss;
+  }
+  if (o != in_bytes) return false;
+  h.ok = true;
+  h.err = 0;
+  return true;
+}
+
 int lopc_decompress_ex(const void* in, size_t in_bytes, void* out, size_t out_capacity, void* workspace,
                        size_t workspace_bytes, void* stream) {
   if (!in) return LOPC_E_ARG;
@@ -757,6 +815,65 @@ int lopc_decompress_ex(const void* in, size_t in_bytes, void* out, size_t out_ca
   Timer tm;
   if ((rc = tm.init(st))) return rc;
   g_stats = lopc_stats{};
+  // Host stream -> host values, per-kernel timing off: a pipeline of up to 4
+  // chunk ranges — H2D of range i's payloads (stream st), k_decode of range i
+  // (side stream, after its H2D), D2H of its values (second side stream,
+  // after its decode) — so the PCIe copies overlap the decode.  Offsets come
+  // from the host copy of the size table (validated as k_chunk_scan would).
+  Hdr hh;
+  std::vector<uint64_t> hoff;
+  if (host_in && host_out && !tm.on && host_stream_plan(static_cast<const uint8_t*>(in), in_bytes, out_capacity, hh, hoff)) {
+    const uint8_t* hin = static_cast<const uint8_t*>(in);
+    uint8_t* dsrc = ws + o_in;
+    uint64_t* doff = reinterpret_cast<uint64_t*>(ws + o_off);
+    const uint32_t C = hh.C;
+    const uint64_t k = hh.dtype ? 8 : 4, W = kChunkBytes / k;
+    CK(cudaMemsetAsync(ws + o_ctr, 0, sizeof(Counters), st));
+    CK(cudaMemcpyAsync(dsrc, hin, kHdrBytes + 8ull * C, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(doff, hoff.data(), 8ull * C, cudaMemcpyHostToDevice, st));
+    CK(cudaEventRecord(di->ev_fork, st));
+    CK(cudaStreamWaitEvent(di->side, di->ev_fork, 0));
+    CK(cudaStreamWaitEvent(di->side2, di->ev_fork, 0));
+    const int K = C < 4 ? (int)C : 4;
+    for (int i = 0; i < K; ++i) {
+      const uint64_t cb = (uint64_t)C * i / K, ce = (uint64_t)C * (i + 1) / K;
+      const uint64_t b0 = hoff[cb], b1 = ce == C ? in_bytes : hoff[ce];
+      CK(cudaMemcpyAsync(dsrc + b0, hin + b0, b1 - b0, cudaMemcpyHostToDevice, st));
+      CK(cudaEventRecord(di->ev_in[i], st));
+      CK(cudaStreamWaitEvent(di->side, di->ev_in[i], 0));
+      DecodeArgs da{};
+      da.in = dsrc;
+      da.in_bytes = in_bytes;
+      da.out = ws + o_out;
+      da.out_cap = out_capacity;
+      da.off = doff + cb;
+      da.table = reinterpret_cast<const uint32_t*>(dsrc + kHdrBytes) + 2 * cb;
+      da.base = dsrc;
+      da.c_begin = cb;
+      da.c_count = ce - cb;
+      da.state_cap = C;
+      da.ctr = reinterpret_cast<Counters*>(ws + o_ctr);
+      da.slab = 1;
+      da.given = hh;
+      unsigned grid = 2u * (unsigned)(di->occ_decode > 0 ? di->occ_decode : 1);
+      if (grid > 2 * (ce - cb)) grid = (unsigned)(2 * (ce - cb));
+      k_decode<<<grid, kCodecThreads, sizeof(DecSmem), di->side>>>(da);
+      CK(cudaGetLastError());
+      CK(cudaEventRecord(di->ev_dec[i], di->side));
+      CK(cudaStreamWaitEvent(di->side2, di->ev_dec[i], 0));
+      const uint64_t e0 = cb * W, e1 = ce * W < hh.n ? ce * W : hh.n;
+      CK(cudaMemcpyAsync(static_cast<uint8_t*>(out) + e0 * k, ws + o_out + e0 * k, (e1 - e0) * k,
+                         cudaMemcpyDeviceToHost, di->side2));
+    }
+    CK(cudaEventRecord(di->ev_out, di->side2));
+    CK(cudaStreamWaitEvent(st, di->ev_out, 0));
+    CK(cudaMemcpyAsync(hc, ws + o_ctr, sizeof(Counters), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    for (int i = 0; i < 16; ++i) g_stats.phase_cycles[i] = hc->phase[i];
+    if ((rc = map_err(hc->err))) return rc;
+    g_stats.launches = (uint32_t)K;
+    return LOPC_OK;
+  }
   tm.mark();  // 0
   const uint8_t* src = static_cast<const uint8_t*>(in);
   if (host_in) {
