@@ -206,14 +206,24 @@ def test_corrupt_streams(ref, gpu):
     x = random_field((30, 200), "f32", "smooth", 3)
     st = ref.compress(x, eps_noa(x, 1e-2))
 
-    def rc_gpu(b):
-        t = torch.from_numpy(np.frombuffer(b, np.uint8).copy()).cuda()
-        out = torch.empty(x.shape, dtype=torch.float32, device="cuda")
+    def rc_one(b, host):
+        t = torch.from_numpy(np.frombuffer(b, np.uint8).copy())
+        t = t.pin_memory() if host else t.cuda()
+        out = torch.empty(x.shape, dtype=torch.float32, device="cpu" if host else "cuda")
+        if host:
+            out = out.pin_memory()
         try:
             gpu.decompress(t, out=out)
             return 0
         except gpu.LopcError as e:
             return e.code
+
+    def rc_gpu(b):
+        """device stream -> device values, and host -> host (the pipelined
+        range path, which validates the table on the host): same code"""
+        r = rc_one(b, False)
+        assert rc_one(b, True) == r
+        return r
 
     assert rc_gpu(st) == 0
     assert rc_gpu(st[:-4]) == ref.decompress_rc(st[:-4], x.shape, x.dtype) == -4
