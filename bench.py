@@ -641,7 +641,8 @@ def main():
         "cpu_baseline_multicore": cpu_omp,
         "e2e": {"value": e2e_val, "unit": "GB/s", "h2d_bytes_per_step": raw + nbytes_stream,
                 "d2h_bytes_per_step": nbytes_stream + raw,
-                "note": "lopc_compress/lopc_decompress on pinned host buffers, staging copies inside the call"},
+                "note": "lopc_compress/lopc_decompress on pinned host buffers: staging copies inside the calls, "
+                         "decompress pipelined over chunk ranges (H2D / decode / D2H overlap)"},
         "gpu_launches": launches_timed,
         "clocks": clk.summary(),
         "notes": "per_kernel/roofline: the library's per-launch events (lopc_set_timing) in a second loop; "
