@@ -791,7 +791,7 @@ struct EncSmem {
 };
 
 template <typename T, int ROLE>
-__global__ void __launch_bounds__(kCodecThreads, LOPC_CODEC_CTAS) k_encode(EncodeArgs a) {
+__global__ void __launch_bounds__(kCodecThreads, ROLE == 2 ? LOPC_SUBS_CTAS : LOPC_CODEC_CTAS) k_encode(EncodeArgs a) {
   using U = typename VT<T>::U;
   using I = typename VT<T>::I;
   constexpr bool SUBS = ROLE == 2;

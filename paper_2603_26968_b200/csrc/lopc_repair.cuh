@@ -67,6 +67,9 @@ struct Geo<2> {
 #ifndef LOPC_SWEEP_CTAS
 #define LOPC_SWEEP_CTAS 3  // k_sweep CTAs per SM (register budget 85; 4 and 5 measured slower)
 #endif
+#ifndef LOPC_SUBS_CTAS
+#define LOPC_SUBS_CTAS 5  // k_encode<T, 2> (subbin stream) CTAs per SM: 48 registers, no spills (1 % faster than 6)
+#endif
 #ifndef LOPC_CODEC_CTAS
 #define LOPC_CODEC_CTAS 6  // k_encode / k_decode CTAs per SM (register budget 40; 4 and 5 measured slower)
 #endif
