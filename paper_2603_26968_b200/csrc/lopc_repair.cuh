@@ -67,6 +67,9 @@ struct Geo<2> {
 #ifndef LOPC_SWEEP_CTAS
 #define LOPC_SWEEP_CTAS 3  // k_sweep CTAs per SM (register budget 85; 4 and 5 measured slower)
 #endif
+#ifndef LOPC_QF_CTAS
+#define LOPC_QF_CTAS 4  // k_quant_flags CTAs (of 512) per SM for f32 (32 registers, no spills: 0.180 -> 0.172 ms on cfg2); f64 keeps 3
+#endif
 #ifndef LOPC_SUBS_CTAS
 #define LOPC_SUBS_CTAS 5  // k_encode<T, 2> (subbin stream) CTAs per SM: 48 registers, no spills (1 % faster than 6)
 #endif
@@ -399,7 +402,7 @@ constexpr size_t quant_flags_smem() {
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
 template <typename T, int NDIM, typename Idx, bool TMA>
-__global__ void __launch_bounds__(kRepairThreads, 3) k_quant_flags(RepairArgs a, const __grid_constant__ CUtensorMap tmap) {
+__global__ void __launch_bounds__(kRepairThreads, sizeof(T) == 4 ? LOPC_QF_CTAS : 3) k_quant_flags(RepairArgs a, const __grid_constant__ CUtensorMap tmap) {
   using G = Geo<NDIM>;
   using I = typename VT<T>::I;
   using U = typename VT<T>::U;
