@@ -328,3 +328,23 @@ def omp_compress(x: np.ndarray, eps: float, threads: int = 0):
     if rc:
         raise OracleError(rc, "omp_compress")
     return out.raw[: nb.value], int(sw.value)
+
+
+def omp_check_chunks(x: np.ndarray, eps: float, s: np.ndarray, stream) -> tuple:
+    """(mismatching chunks, first bad chunk or None): every chunk of `stream`
+    against the oracle's chunk encoder on (x, eps, s), all host cores
+    (lopc_omp_check_chunks).  s must be certified first (certify(x, eps, s)
+    == 0), which makes the expected bytes the oracle's stream."""
+    global _omp
+    if _omp is None:
+        omp_compress(np.zeros((1, 1), np.float32), 1.0)  # loads the library
+    f = _omp.lopc_omp_check_chunks
+    f.argtypes = [C.c_void_p, C.c_uint64, C.c_int, C.c_double, C.c_void_p, C.c_void_p, C.c_uint64,
+                  C.POINTER(C.c_uint64)]
+    f.restype = C.c_uint64
+    x = np.ascontiguousarray(x)
+    s = np.ascontiguousarray(s, dtype=np.uint32)
+    st = np.frombuffer(stream, np.uint8) if isinstance(stream, (bytes, bytearray)) else np.ascontiguousarray(stream)
+    first = C.c_uint64()
+    bad = int(f(_ptr(x), x.size, _dt(x), float(eps), _ptr(s), _ptr(st), st.size, C.byref(first)))
+    return bad, (None if first.value == 2**64 - 1 else int(first.value))

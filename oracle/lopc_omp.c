@@ -142,3 +142,75 @@ int lopc_omp_compress(const void* x, int ndims, const uint64_t* dims, int dtype,
   free(sz);
   return rc;
 }
+
+/* Whole-stream chunk check for fields too large for the single-thread oracle
+ * (cfg5 rank slab, 1 G points): every chunk c is encoded by the oracle's own
+ * chunk encoder (lopc_ref_encode_chunk, a5/a6) from (x, eps, s) and compared
+ * byte for byte with the stream under test: its size-table entry and its
+ * payloads at the offsets the table's exclusive scan gives (a7), plus the
+ * header fields and the total length.  s must already be certified as the
+ * least fixpoint by lopc_ref_certify (O9: the Bellman certificate proves it
+ * IS the oracle's subbins), which makes this the oracle's stream.  Returns the
+ * number of mismatching chunks (+1 for a header / length mismatch), or
+ * (uint64_t)-1 on allocation failure; the first bad chunk index goes to
+ * *first_bad (or UINT64_MAX). */
+uint64_t lopc_omp_check_chunks(const void* x, uint64_t n, int dtype, double eps, const uint32_t* s,
+                               const void* stream, uint64_t stream_bytes, uint64_t* first_bad) {
+  const int k = dtype ? 8 : 4;
+  const uint64_t W = 16384 / k, C = (n + W - 1) / W;
+  const uint8_t* st = (const uint8_t*)stream;
+  *first_bad = UINT64_MAX;
+  uint64_t bad = 0;
+  if (stream_bytes < 64 + 8 * C) return 1 + C;
+  uint64_t hn, htotal;
+  uint32_t hc;
+  double heps;
+  memcpy(&hn, st + 40, 8);
+  memcpy(&hc, st + 52, 4);
+  memcpy(&htotal, st + 56, 8);
+  memcpy(&heps, st + 32, 8);
+  if (memcmp(st, "LOPC", 4) || hn != n || hc != C || htotal != stream_bytes || heps != eps || st[6] != dtype) bad++;
+  uint64_t* off = malloc(8 * (C ? C : 1));
+  if (!off) return (uint64_t)-1;
+  uint64_t o = 64 + 8 * C;
+  for (uint64_t c = 0; c < C; c++) {
+    uint32_t bs, ss;
+    memcpy(&bs, st + 64 + 8 * c, 4);
+    memcpy(&ss, st + 64 + 8 * c + 4, 4);
+    off[c] = o;
+    o += (uint64_t)bs + ss;
+  }
+  if (o != stream_bytes) bad++;
+  uint64_t first = UINT64_MAX;
+#pragma omp parallel
+  {
+    uint8_t* buf = malloc(32768);
+    uint64_t my_first = UINT64_MAX, my_bad = 0;
+#pragma omp for schedule(dynamic, 64)
+    for (int64_t ci = 0; ci < (int64_t)C; ci++) {
+      const uint64_t c = (uint64_t)ci;
+      uint32_t sz[2];
+      int ok = buf && lopc_ref_encode_chunk(x, n, dtype, eps, s, c, buf, sz) == 0;
+      if (ok) {
+        uint32_t bs, ss;
+        memcpy(&bs, st + 64 + 8 * c, 4);
+        memcpy(&ss, st + 64 + 8 * c + 4, 4);
+        ok = bs == sz[0] && ss == sz[1] && off[c] + bs + ss <= stream_bytes &&
+             memcmp(st + off[c], buf, (size_t)bs + ss) == 0;
+      }
+      if (!ok) {
+        my_bad++;
+        if (c < my_first) my_first = c;
+      }
+    }
+#pragma omp critical
+    {
+      bad += my_bad;
+      if (my_first < first) first = my_first;
+    }
+    free(buf);
+  }
+  *first_bad = first;
+  free(off);
+  return bad;
+}

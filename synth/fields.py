@@ -170,6 +170,26 @@ def random_field(dims, dtype="f32", kind="noise", seed=0) -> np.ndarray:
         f = -np.arange(int(np.prod(dims)), dtype=np.float64).reshape(dims) * 1e-3
     elif kind == "grid16":
         f = np.round(rng.standard_normal(dims) * 16.0) / 16.0
+    elif kind == "signed_zero_subnormal":
+        # bin 0 crowded with -0.0 beside +0.0 (equal values: ties by index,
+        # G13), subnormals of both signs and tiny normals, inside a smooth
+        # field of range ~1 (so NOA eps stays a normal number)
+        f = _grf(dims, 3.0, rng).astype(np.float64) if min(dims) > 1 else rng.standard_normal(dims)
+        f = (f / max(1e-30, float(np.abs(f).max()))).astype(dt)
+        u = np.dtype(dt).itemsize * 8
+        ut = np.uint32 if u == 32 else np.uint64
+        mant = (1 << (23 if u == 32 else 52)) - 1
+        sub = (rng.integers(1, mant, size=dims, dtype=np.uint64).astype(ut)).view(dt)  # positive subnormals
+        tiny = np.finfo(dt).tiny
+        pick = rng.integers(0, 8, size=dims)
+        sign = np.where(rng.random(dims) < 0.5, -1.0, 1.0).astype(dt)
+        choice = [np.zeros(dims, dt), -np.zeros(dims, dt), sub, -sub,
+                  np.full(dims, np.finfo(dt).smallest_subnormal, dt) * sign, np.full(dims, tiny, dt) * sign,
+                  sub * sign, f]
+        g = np.choose(pick, choice)
+        mask = rng.random(dims) < 0.6
+        f = np.where(mask, g, f)
+        return np.ascontiguousarray(f.astype(dt))
     else:
         raise ValueError(kind)
     return np.ascontiguousarray(f.astype(dt))

@@ -234,3 +234,50 @@ def same_bin_components(field: np.ndarray, bins):
                     stack.append(q)
         cid += 1
     return comp
+
+
+# --- RZE_g written from the stream-format text --
+def rze_spec(data: bytes, g: int) -> bytes:
+    """Repeated zero-byte elimination, restated from the format text and
+    nothing else: the paper's "bitmap ... repeatedly compressed with a similar
+    algorithm that identifies repeating words" (§IV.C, Fig. 2) as the
+    container reads it (reading G21).
+
+    * n = L/g words; bitmap B0 has ceil(n/8) bytes, bit i (LSB-first) says
+      word i is not all zero.
+    * while |B_i| > 8: B_{i+1} has ceil(|B_i|/8) bytes, bit t says
+      B_i[t] differs from B_i[t-1] (B_i[-1] = 0); K_i lists, in order, the
+      bytes B_i[t] whose bit t is set.
+    * output = B_top, then K_{top-1}, ..., K_0, then the non-zero words.
+
+    Written with explicit bit lists (no shifts shared with the oracle's
+    packing), so a swapped level order, a "!= 0" instead of "!= previous"
+    repeat test, or an MSB-first bitmap changes the bytes."""
+    assert len(data) % g == 0
+    words = [data[i:i + g] for i in range(0, len(data), g)]
+    nonzero = [any(w) for w in words]
+
+    def pack(bits):
+        out = []
+        for i in range(0, len(bits), 8):
+            byte = 0
+            for j, b in enumerate(bits[i:i + 8]):
+                if b:
+                    byte += 2 ** j
+            out.append(byte)
+        return out
+
+    levels = [pack(nonzero)]          # B0
+    kept = []                         # K0, K1, ...
+    while len(levels[-1]) > 8:
+        b = levels[-1]
+        rep = [b[t] != (b[t - 1] if t > 0 else 0) for t in range(len(b))]
+        kept.append([b[t] for t in range(len(b)) if rep[t]])
+        levels.append(pack(rep))
+    out = list(levels[-1])
+    for k in reversed(kept):
+        out += k
+    for w, nz in zip(words, nonzero):
+        if nz:
+            out += list(w)
+    return bytes(out)

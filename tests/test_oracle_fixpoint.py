@@ -100,7 +100,7 @@ def test_spec_two_point_examples(ref):
 
 CASES = []
 for seed in range(60):
-    for kind in ("noise", "ties", "plateau", "grid16", "smooth"):
+    for kind in ("noise", "ties", "plateau", "grid16", "smooth", "signed_zero_subnormal"):
         CASES.append((seed, kind))
 
 

@@ -23,7 +23,7 @@ def _exact_bound_ok(x, y, eps):
     return True
 
 
-CASES = [(seed, kind, rel) for seed in range(8) for kind in ("noise", "smooth", "ties", "plateau", "grid16")
+CASES = [(seed, kind, rel) for seed in range(8) for kind in ("noise", "smooth", "ties", "plateau", "grid16", "signed_zero_subnormal")
          for rel in (0.1, 0.01)]
 
 

@@ -28,3 +28,27 @@ def test_omp_chain_and_config(ref):
     y = cfg.generate((180, 360))
     eps = eps_noa(y, cfg.rel)
     assert ref.omp_compress(y, eps)[0] == ref.compress(y, eps)
+
+
+def test_omp_check_chunks_teeth(ref):
+    """lopc_omp_check_chunks (the whole-stream check used for the cfg5 rank
+    slab) accepts the oracle's stream and finds a flipped payload byte, a
+    wrong subbin and a wrong header field."""
+    import struct
+
+    from synth.fields import CONFIGS, eps_noa
+
+    x = CONFIGS["cfg2"].generate((20, 100, 100))
+    eps = eps_noa(x, 1e-3)
+    st = ref.compress(x, eps)
+    s = ref.subbins(x, eps)
+    assert ref.omp_check_chunks(x, eps, s, st) == (0, None)
+    b = bytearray(st)
+    b[-5] ^= 1
+    assert ref.omp_check_chunks(x, eps, s, bytes(b)) == (1, 48)
+    s2 = s.copy()
+    s2.ravel()[5000] += 1
+    assert ref.omp_check_chunks(x, eps, s2, st) == (1, 1)
+    h = bytearray(st)
+    struct.pack_into("<d", h, 32, eps * 2)
+    assert ref.omp_check_chunks(x, eps, s, bytes(h))[0] == 1

@@ -171,3 +171,92 @@ def test_errors(ref):
     struct.pack_into("<I", t, 64, 6)  # bin size no longer matches the payload
     assert ref.decompress_rc(bytes(t), x.shape, x.dtype) == -4
     assert ref.decompress_rc(st[:10], x.shape, x.dtype) == -4
+
+
+def test_rze_two_level_hand_vector(ref):
+    """RZE_1 of 1024 bytes, zero except d[100] = 0x09, d[900] = 0x41,
+    d[901] = 0x42, derived by hand from the format text (reading G21):
+      B0 (128 B): B0[12] = 0x10 (word 100), B0[112] = 0x30 (words 900, 901)
+      B1 (16 B):  B0 changes at t = 12, 13, 112, 113 -> B1[1] = 0x30, B1[14] = 0x03
+      K0 = B0[12], B0[13], B0[112], B0[113] = 10 00 30 00
+      B2 (2 B):   B1 changes at t = 1, 2, 14, 15 -> B2 = 06 c0 (|B2| <= 8: top)
+      K1 = B1[1], B1[2], B1[14], B1[15] = 30 00 03 00
+      output = B2 | K1 | K0 | words = 06 c0 | 30 00 03 00 | 10 00 30 00 | 09 41 42
+    B0[13] = 0 is kept only because it differs from B0[12]: a "!= 0" repeat
+    test would drop it."""
+    from tests.exact import rze_spec
+
+    d = bytearray(1024)
+    d[100], d[900], d[901] = 0x09, 0x41, 0x42
+    want = bytes.fromhex("06c0" "30000300" "10003000" "094142")
+    assert rze_spec(bytes(d), 1) == want
+    assert ref.rze(bytes(d), 1) == want
+    out, used = ref.unrze(want, 1024, 1)
+    assert out == bytes(d) and used == len(want)
+
+
+@pytest.mark.parametrize("g", [1, 4, 8])
+def test_rze_matches_spec(ref, g):
+    """The oracle's RZE_g equals the independent restatement (tests/exact.py
+    rze_spec) on 16384-byte inputs whose bitmap levels have non-empty K_1 /
+    K_2 (clustered runs of non-zero words at several densities), plus short
+    inputs; >= 100 cases per g."""
+    from tests.exact import rze_spec
+
+    rng = np.random.default_rng(100 + g)
+    deep = 0
+    for trial in range(110):
+        L = 16384 if trial % 4 else int(rng.integers(1, 600)) * g
+        n = L // g
+        kind = trial % 5
+        w = np.zeros((n, g), np.uint8)
+        if kind == 0:      # sparse isolated words
+            idx = rng.choice(n, size=max(1, n // 200), replace=False)
+            w[idx] = rng.integers(1, 256, (idx.size, g))
+        elif kind == 1:    # runs of non-zero words (B0 bytes 0xff inside runs)
+            for _ in range(int(rng.integers(1, 20))):
+                a = int(rng.integers(0, n))
+                w[a:a + int(rng.integers(1, 300))] = rng.integers(1, 256, g)
+        elif kind == 2:    # dense random words with zero holes
+            w[:] = rng.integers(0, 256, (n, g))
+            w[rng.random(n) < 0.3] = 0
+        elif kind == 3:    # periodic patterns (B0 repeats a non-zero byte)
+            per = int(rng.integers(2, 17))
+            w[::per] = rng.integers(1, 256, g)
+        else:              # mostly zero with a few partially-zero words
+            idx = rng.choice(n, size=max(1, n // 50), replace=False)
+            w[idx, int(rng.integers(0, g))] = rng.integers(1, 256, idx.size)
+        data = w.tobytes()
+        enc = ref.rze(data, g)
+        assert enc == rze_spec(data, g), (g, trial, kind)
+        nb0 = -(-n // 8)
+        if nb0 > 64:
+            deep += 1
+    assert deep >= 60  # most cases recurse at least twice (|B0| > 64 bytes)
+
+
+def test_bound_violations_teeth(ref):
+    """The exact bound checker (O13; proof (i): 0 <= x - x^ <= eps)
+    fires one ulp past the bound, on the wrong side, and on a changed escape;
+    the TwoSum term decides a difference that rounds to exactly eps."""
+    up, dn = (lambda v: np.nextafter(v, np.inf)), (lambda v: np.nextafter(v, -np.inf))
+    x = np.array([1.0])
+    assert ref.bound_violations(x, np.array([0.75]), 0.25) == 0          # exactly eps below
+    assert ref.bound_violations(x, np.array([dn(0.75)]), 0.25) == 1      # one ulp past eps
+    assert ref.bound_violations(x, np.array([1.0]), 0.25) == 0
+    assert ref.bound_violations(x, np.array([up(1.0)]), 0.25) == 1       # above x: one-sided error
+    # 8 - (-2^-60) = 8 + 2^-60 rounds to 8 = eps but exceeds it; 8 - 2^-60 does not
+    assert ref.bound_violations(np.array([8.0]), np.array([-2.0 ** -60]), 8.0) == 1
+    assert ref.bound_violations(np.array([8.0]), np.array([2.0 ** -60]), 8.0) == 0
+    # f32: one f32 ulp past eps
+    xf = np.array([1.0], np.float32)
+    assert ref.bound_violations(xf, np.array([0.75], np.float32), 0.25) == 0
+    assert ref.bound_violations(xf, np.array([np.nextafter(np.float32(0.75), np.float32(0))]), 0.25) == 1
+    # escapes must come back bitwise
+    xe = np.array([np.inf, np.nan, 1e300])
+    assert ref.bound_violations(xe, xe.copy(), 1e-3) == 0
+    assert ref.bound_violations(xe, np.array([np.inf, np.nan, up(1e300)]), 1e-3) == 1
+    assert ref.bound_violations(xe, np.array([-np.inf, np.nan, 1e300]), 1e-3) == 1
+    # counts add up over points
+    xs = np.array([1.0, 2.0, 3.0])
+    assert ref.bound_violations(xs, np.array([dn(0.75), 2.0, up(3.0)]), 0.25) == 2
