@@ -1,13 +1,13 @@
 """bench.py — LOPC hot path on B200: compress + decompress throughput.
 
-One step = one pass of the whole hot path over one
+One step (default cfg3, 512^3 f32) = one pass of the whole hot path over one
 synthetic field: lopc_compress (quantize -> repair to the fixpoint -> chunked
 encode with look-back placement) followed by lopc_decompress, input resident
 in HBM.  value = raw input GB (all ranks) / (max over ranks of the summed
 device time of the K timed steps), in GB/s.  L2 (126 MB) is flushed between
 steps by writing a 512 MB buffer outside the timed events.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg2]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg3]
   python bench.py --impl reference ...   # the CPU oracle arm (rank 0 only)
 
 Multi-GPU (torchrun): the slab mode — one global field, the
@@ -133,43 +133,53 @@ def oracle_sample(cfg_name: str, x: np.ndarray, eps: float, budget_s: float):
     oracle.build()
     planes = crop_planes(x)
     crop = np.ascontiguousarray(x[:planes])
-    t0 = time.perf_counter()
-    done = 0
-    reps = 0
-    while True:
-        st = oracle.compress(crop, eps)
-        oracle.decompress(st)
-        done += crop.nbytes
-        reps += 1
-        if time.perf_counter() - t0 > budget_s:
-            break
-    dt = time.perf_counter() - t0
+    allowed = sorted(os.sched_getaffinity(0))
+    core = allowed[-1]
+    os.sched_setaffinity(0, {core})  # one thread, pinned
+    try:
+        t0 = time.perf_counter()
+        done = 0
+        reps = 0
+        while True:
+            st = oracle.compress(crop, eps)
+            oracle.decompress(st)
+            done += crop.nbytes
+            reps += 1
+            if time.perf_counter() - t0 > budget_s:
+                break
+        dt = time.perf_counter() - t0
+    finally:
+        os.sched_setaffinity(0, set(allowed))
     desc = (f"oracle compress+decompress of the leading {planes} of {x.shape[0]} "
-            f"{'z-planes' if x.ndim == 3 else 'rows'} of {cfg_name} ({crop.nbytes / 1e6:.1f} MB) x{reps}, "
-            f"{dt:.1f} s, 1 thread on {cpu_model()}")
+            f"{'z-planes' if x.ndim == 3 else 'rows'} of {cfg_name} ({crop.nbytes / 1e6:.1f} MB, a crop) x{reps}, "
+            f"{dt:.1f} s, 1 thread pinned to core {core} of {os.cpu_count()} on {cpu_model()}; "
+            f"full-size single-thread timings: tools/oracle_timing.py -> results/")
     return done / dt / 1e9, desc
 
 
 def omp_sample(cfg_name: str, x: np.ndarray, eps: float, budget_s: float):
     """NEXT f4: the OpenMP CPU baseline (oracle/lopc_omp.c, all host cores) on
-    the same bounded crop, compress only (GB/s of raw input)."""
+    the same bounded crop, compress + decompress (GB/s of raw input), the
+    same round trip as cpu_baseline."""
     import oracle
 
     planes = crop_planes(x)
     crop = np.ascontiguousarray(x[:planes])
     st, _ = oracle.omp_compress(crop, eps)  # warm-up (thread pool, build)
+    oracle.omp_decompress(st)
     t0 = time.perf_counter()
     reps = 0
     while True:
         st, sweeps = oracle.omp_compress(crop, eps)
+        oracle.omp_decompress(st)
         reps += 1
         if time.perf_counter() - t0 > budget_s:
             break
     dt = time.perf_counter() - t0
-    return {"value": crop.nbytes * reps / dt / 1e9, "unit": "GB/s", "cores": os.cpu_count(), "kind": "oracle_omp",
-            "metric": "compress only",
-            "sample": f"OpenMP compress of the leading {planes} of {x.shape[0]} planes of {cfg_name} "
-                      f"({crop.nbytes / 1e6:.1f} MB) x{reps}, {sweeps} relaxation sweeps, {cpu_model()}"}
+    return {"value": crop.nbytes * reps / dt / 1e9, "unit": "GB/s", "cores": len(os.sched_getaffinity(0)),
+            "kind": "oracle_omp", "metric": "compress + decompress",
+            "sample": f"OpenMP compress+decompress of the leading {planes} of {x.shape[0]} planes of {cfg_name} "
+                      f"({crop.nbytes / 1e6:.1f} MB, a crop) x{reps}, {sweeps} relaxation sweeps, {cpu_model()}"}
 
 
 def cfg5_eps(world: int) -> float:
@@ -423,7 +433,9 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="cfg2", choices=sorted(WORKLOAD))
+    # cfg3 (512^3 f32): the largest single-GPU config of BASELINE.json (cfg5
+    # is the 8-GPU one); its metric names no config, so the bench line is on it
+    ap.add_argument("--config", default="cfg3", choices=sorted(WORKLOAD))
     ap.add_argument("--impl", default="lopc", choices=["lopc", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0)

@@ -348,3 +348,20 @@ def omp_check_chunks(x: np.ndarray, eps: float, s: np.ndarray, stream) -> tuple:
     first = C.c_uint64()
     bad = int(f(_ptr(x), x.size, _dt(x), float(eps), _ptr(s), _ptr(st), st.size, C.byref(first)))
     return bad, (None if first.value == 2**64 - 1 else int(first.value))
+
+
+def omp_decompress(stream: bytes, threads: int = 0) -> np.ndarray:
+    """The OpenMP decompress (every chunk in parallel by lopc_ref_decode_chunk)."""
+    global _omp
+    if _omp is None:
+        omp_compress(np.zeros((1, 1), np.float32), 1.0)
+    f = _omp.lopc_omp_decompress
+    f.argtypes = [C.c_void_p, C.c_size_t, C.c_void_p, C.c_size_t, C.c_int]
+    f.restype = C.c_int
+    info = stream_info(stream)
+    out = np.empty(info["shape"], np.float32 if info["dtype"] == 0 else np.float64)
+    buf = np.frombuffer(stream, np.uint8)
+    rc = f(_ptr(buf), len(stream), _ptr(out), out.nbytes, int(threads))
+    if rc:
+        raise OracleError(rc, "omp_decompress")
+    return out

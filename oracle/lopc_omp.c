@@ -214,3 +214,43 @@ uint64_t lopc_omp_check_chunks(const void* x, uint64_t n, int dtype, double eps,
   free(off);
   return bad;
 }
+
+/* Multi-core decompress (f4 baseline, paired with lopc_omp_compress so the
+ * two CPU baselines time the same round trip): header parse and the size
+ * table's exclusive scan serially, then every chunk by lopc_ref_decode_chunk
+ * in parallel.  Same return codes as lopc_ref_decompress. */
+int lopc_omp_decompress(const void* in, size_t in_bytes, void* out, size_t out_capacity, int threads) {
+  if (threads > 0) omp_set_num_threads(threads);
+  int nd, dt;
+  uint64_t d3[3], n;
+  uint32_t C;
+  double eps;
+  int rc = lopc_ref_stream_info(in, in_bytes, &nd, d3, &dt, &eps, &n, &C);
+  if (rc) return rc;
+  const int k = dt ? 8 : 4;
+  if (out_capacity < n * (uint64_t)k) return -3;
+  const uint8_t* st = (const uint8_t*)in;
+  uint64_t* off = malloc(8 * (C ? C : 1));
+  uint32_t* sz = malloc(8 * (C ? C : 1));
+  if (!off || !sz) return -8;
+  uint64_t o = 64 + 8ull * C;
+  for (uint32_t c = 0; c < C; c++) {
+    memcpy(sz + 2 * c, st + 64 + 8ull * c, 8);
+    if (sz[2 * c] < 4 || sz[2 * c] > 16384 || (sz[2 * c] & 3) || sz[2 * c + 1] < 4 || sz[2 * c + 1] > 16384 ||
+        (sz[2 * c + 1] & 3))
+      rc = -4;
+    off[c] = o;
+    o += (uint64_t)sz[2 * c] + sz[2 * c + 1];
+  }
+  if (!rc && o != in_bytes) rc = -4;
+  if (!rc) {
+    int bad = 0;
+#pragma omp parallel for schedule(dynamic, 16) reduction(| : bad)
+    for (int64_t c = 0; c < (int64_t)C; c++)
+      if (lopc_ref_decode_chunk(st + off[c], sz[2 * c], sz[2 * c + 1], (uint32_t)c, n, dt, eps, out)) bad = 1;
+    if (bad) rc = -4;
+  }
+  free(off);
+  free(sz);
+  return rc;
+}

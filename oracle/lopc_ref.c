@@ -904,6 +904,66 @@ int lopc_ref_chunk_sizes(const void* in, size_t nbytes, uint32_t* sizes, uint32_
   return 0;
 }
 
+/* O12, one chunk: inverse stages of chunk c's two payloads (q: bin payload
+ * of bs bytes, then the subbin payload of ss bytes), then O10 for its
+ * elements [cW, min((c+1)W, n)) into out (the whole field's buffer). */
+static int decode_one_chunk(const uint8_t* q, uint32_t bs, uint32_t ss, uint32_t c, uint64_t n, int dt,
+                            double eps, void* out, uint8_t* bw, uint8_t* sw, uint8_t* t1, uint8_t* t2) {
+  int k = dt == 0 ? 4 : 8;
+  uint64_t W = CHUNK_BYTES / (uint64_t)k;
+  /* bins */
+  if (bs == CHUNK_BYTES) {
+    memcpy(bw, q, CHUNK_BYTES);
+  } else {
+    long used = lopc_ref_unrze(q, bs, CHUNK_BYTES, 1, t1);
+    if (used < 0 || pad4((size_t)used) != bs) return E_CORRUPT;
+    lopc_ref_unbitshuffle(t1, W, k, t2);
+    lopc_ref_undiffnb(t2, W, k, bw);
+  }
+  q += bs;
+  /* subbins */
+  if (ss == CHUNK_BYTES) {
+    memcpy(sw, q, CHUNK_BYTES);
+  } else {
+    size_t l1 = get_u16(q);
+    size_t l1max = CHUNK_BYTES + CHUNK_BYTES / (size_t)k / 8 + 64 + 8;
+    if (l1 > l1max) return E_CORRUPT;
+    long used = lopc_ref_unrze(q + 2, ss - 2, l1, 1, t1);
+    if (used < 0 || pad4(2 + (size_t)used) != ss) return E_CORRUPT;
+    long used2 = lopc_ref_unrze(t1, l1, CHUNK_BYTES, k, t2);
+    if (used2 < 0 || (size_t)used2 != l1) return E_CORRUPT;
+    lopc_ref_unbitshuffle(t2, W, k, sw);
+  }
+  /* O10 per element */
+  for (uint64_t i = c * W; i < n && i < (c + 1) * W; i++) {
+    uint64_t bwv = word_get(bw + (i - c * W) * k, k);
+    uint64_t swv = word_get(sw + (i - c * W) * k, k);
+    uint64_t v;
+    if (bwv == (dt == 0 ? 0x80000000ull : 0x8000000000000000ull)) {
+      v = swv;
+    } else {
+      int64_t b = dt == 0 ? (int64_t)(int32_t)(uint32_t)bwv : (int64_t)bwv;
+      v = decode_point(b, swv, eps, dt);
+    }
+    memcpy((uint8_t*)out + (size_t)k * i, &v, (size_t)k);
+  }
+  return 0;
+}
+
+int lopc_ref_decode_chunk(const void* payloads, uint32_t bin_size, uint32_t sub_size, uint32_t c, uint64_t n,
+                          int dtype, double eps, void* out) {
+  uint8_t *bw = (uint8_t*)malloc(CHUNK_BYTES), *sw = (uint8_t*)malloc(CHUNK_BYTES);
+  uint8_t *t1 = (uint8_t*)malloc(2 * CHUNK_BYTES), *t2 = (uint8_t*)malloc(2 * CHUNK_BYTES);
+  int rc = (!bw || !sw || !t1 || !t2)
+               ? E_INTERNAL
+               : decode_one_chunk((const uint8_t*)payloads, bin_size, sub_size, c, n, dtype, eps, out, bw, sw, t1, t2);
+  free(bw);
+  free(sw);
+  free(t1);
+  free(t2);
+  return rc;
+}
+
 /* O12: parse, offsets = exclusive scan of sizes, inverse stages, O10. */
 int lopc_ref_decompress(const void* in, size_t in_bytes, void* out, size_t out_capacity) {
   int nd, dt;
@@ -923,7 +983,6 @@ int lopc_ref_decompress(const void* in, size_t in_bytes, void* out, size_t out_c
     total += sz;
   }
   if (total != in_bytes) return E_CORRUPT;
-  uint64_t W = CHUNK_BYTES / (uint64_t)k;
   uint8_t *bw = (uint8_t*)malloc(CHUNK_BYTES), *sw = (uint8_t*)malloc(CHUNK_BYTES);
   uint8_t *t1 = (uint8_t*)malloc(2 * CHUNK_BYTES), *t2 = (uint8_t*)malloc(2 * CHUNK_BYTES);
   if (!bw || !sw || !t1 || !t2) {
@@ -933,55 +992,9 @@ int lopc_ref_decompress(const void* in, size_t in_bytes, void* out, size_t out_c
   const uint8_t* q = p + HDR_BYTES + 8ull * C;
   for (uint32_t c = 0; c < C; c++) {
     uint32_t bs = get_u32(tab + 8 * c), ss = get_u32(tab + 8 * c + 4);
-    /* bins */
-    if (bs == CHUNK_BYTES) {
-      memcpy(bw, q, CHUNK_BYTES);
-    } else {
-      long used = lopc_ref_unrze(q, bs, CHUNK_BYTES, 1, t1);
-      if (used < 0 || pad4((size_t)used) != bs) {
-        rc = E_CORRUPT;
-        goto out;
-      }
-      lopc_ref_unbitshuffle(t1, W, k, t2);
-      lopc_ref_undiffnb(t2, W, k, bw);
-    }
-    q += bs;
-    /* subbins */
-    if (ss == CHUNK_BYTES) {
-      memcpy(sw, q, CHUNK_BYTES);
-    } else {
-      size_t l1 = get_u16(q);
-      size_t l1max = CHUNK_BYTES + CHUNK_BYTES / (size_t)k / 8 + 64 + 8;
-      if (l1 > l1max) {
-        rc = E_CORRUPT;
-        goto out;
-      }
-      long used = lopc_ref_unrze(q + 2, ss - 2, l1, 1, t1);
-      if (used < 0 || pad4(2 + (size_t)used) != ss) {
-        rc = E_CORRUPT;
-        goto out;
-      }
-      long used2 = lopc_ref_unrze(t1, l1, CHUNK_BYTES, k, t2);
-      if (used2 < 0 || (size_t)used2 != l1) {
-        rc = E_CORRUPT;
-        goto out;
-      }
-      lopc_ref_unbitshuffle(t2, W, k, sw);
-    }
-    q += ss;
-    /* O10 per element */
-    for (uint64_t i = c * W; i < n && i < (c + 1) * W; i++) {
-      uint64_t bwv = word_get(bw + (i - c * W) * k, k);
-      uint64_t swv = word_get(sw + (i - c * W) * k, k);
-      uint64_t v;
-      if (bwv == (dt == 0 ? 0x80000000ull : 0x8000000000000000ull)) {
-        v = swv;
-      } else {
-        int64_t b = dt == 0 ? (int64_t)(int32_t)(uint32_t)bwv : (int64_t)bwv;
-        v = decode_point(b, swv, eps, dt);
-      }
-      memcpy((uint8_t*)out + (size_t)k * i, &v, (size_t)k);
-    }
+    rc = decode_one_chunk(q, bs, ss, c, n, dt, eps, out, bw, sw, t1, t2);
+    if (rc) goto out;
+    q += bs + ss;
   }
 out:
   free(bw);

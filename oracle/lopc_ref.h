@@ -74,6 +74,12 @@ int lopc_ref_chunk_sizes(const void* in, size_t n, uint32_t* sizes, uint32_t cap
 int lopc_ref_encode_chunk(const void* x, uint64_t n, int dtype, double eps, const uint32_t* s, uint64_t c,
                           void* out, uint32_t* sizes2);
 
+/* O12 for one chunk c: payloads = its bin payload (bin_size bytes) then its
+ * subbin payload (sub_size bytes); writes elements [cW, min((c+1)W, n)) of
+ * out (the whole field's buffer).  0 or E_CORRUPT / E_INTERNAL. */
+int lopc_ref_decode_chunk(const void* payloads, uint32_t bin_size, uint32_t sub_size, uint32_t c, uint64_t n,
+                          int dtype, double eps, void* out);
+
 /* --- Lossless stages (G17-G21) ---------------------- */
 void lopc_ref_diffnb(const void* words, size_t W, int k, void* out);
 void lopc_ref_undiffnb(const void* in, size_t W, int k, void* words);

@@ -52,3 +52,18 @@ def test_omp_check_chunks_teeth(ref):
     h = bytearray(st)
     struct.pack_into("<d", h, 32, eps * 2)
     assert ref.omp_check_chunks(x, eps, s, bytes(h))[0] == 1
+
+
+def test_omp_decompress_equals_oracle(ref):
+    """The OpenMP decompress (chunks in parallel through the oracle's own
+    per-chunk decoder) gives the oracle's bits; corrupt streams fail."""
+    from synth.fields import CONFIGS, eps_noa, random_field
+
+    for x in (CONFIGS["cfg2"].generate((20, 100, 100)), random_field((70, 300), "f64", "smooth", 3)):
+        eps = eps_noa(x, 1e-3)
+        st = ref.compress(x, eps)
+        assert ref.omp_decompress(st).tobytes() == ref.decompress(st).tobytes()
+        import oracle
+
+        with pytest.raises(oracle.OracleError):
+            ref.omp_decompress(st[:-4])
