@@ -12,6 +12,7 @@
 
 #include <cmath>
 #include <cstdlib>
+#include <mutex>
 #include <cstdio>
 #include <cstring>
 #include <vector>
@@ -19,6 +20,7 @@
 #include "../../include/lopc.h"
 #include "lopc_codec.cuh"
 #include "lopc_repair.cuh"
+#include "lopc_tiles.cuh"
 #include "lopc_noa.cuh"
 #include "lopc_check.cuh"
 
@@ -26,10 +28,17 @@ using namespace lopc;
 
 namespace {
 
-char g_errmsg[512] = "";
-lopc_stats g_stats{};
+// Concurrency (calls on different streams or workspaces are
+// independent): everything a call writes on the host side is per thread —
+// the error text, the stats, the pinned status slot, the side streams and
+// events, the timing events, the plain calls' workspace pool — and keyed by
+// device.  Only configuration (lopc_set_timing / lopc_set_repair_engine) and
+// the once-initialised TMA entry point are process-wide.
+thread_local char g_errmsg[512] = "";
+thread_local lopc_stats g_stats{};
 int g_timing = 0;
 int g_engine = 0;  // lopc_set_repair_engine
+constexpr int kMaxDev = 64;
 
 int set_cuda_error(cudaError_t e, const char* where) {
   snprintf(g_errmsg, sizeof(g_errmsg), "%s: %s (%s)", where, cudaGetErrorName(e), cudaGetErrorString(e));
@@ -87,10 +96,13 @@ float inv32_of(double eps) {
 }
 
 struct CLayout {
-  size_t ctr, bitmap, state, zero_end, plist, flags, s, stage, sizes, off, stage_in, stage_out, total;
+  size_t ctr, bitmap, state, act0, act1, zero_end, plist, flags, s, sp, list0, list1, stage, sizes, off, stage_in,
+      stage_out, total;
   uint64_t bmw, nseg;
   int ntz, nty, ntx;
   uint64_t ntiles;
+  uint32_t tnt[2][3];  // k_tiles: tiles per axis of tiling 0 / 1
+  uint64_t tn[2];
 };
 
 CLayout compress_layout(const Shape& s, bool host_in, bool host_out) {
@@ -105,6 +117,18 @@ CLayout compress_layout(const Shape& s, bool host_in, bool host_out) {
     L.ntx = (int)((s.d2 + Geo<2>::TX - 1) / Geo<2>::TX);
   }
   L.ntiles = s.n ? (uint64_t)L.ntz * L.nty * L.ntx : 0;
+  {
+    using B3 = TBox<3>;
+    using B2 = TBox<2>;
+    const uint64_t TZ = s.ndims == 3 ? Geo<3>::TZ : 1, TY = s.ndims == 3 ? Geo<3>::TY : Geo<2>::TY;
+    const uint64_t SZ = s.ndims == 3 ? B3::SZ : 0, SY = s.ndims == 3 ? B3::SY : B2::SY;
+    L.tnt[0][0] = (uint32_t)((s.d0 + TZ - 1) / TZ);
+    L.tnt[0][1] = (uint32_t)((s.d1 + TY - 1) / TY);
+    L.tnt[1][0] = (uint32_t)((s.d0 + SZ + TZ - 1) / TZ);
+    L.tnt[1][1] = (uint32_t)((s.d1 + SY + TY - 1) / TY);
+    L.tnt[0][2] = L.tnt[1][2] = (uint32_t)((s.d2 + 31) / 32);
+    for (int t = 0; t < 2; ++t) L.tn[t] = s.n ? (uint64_t)L.tnt[t][0] * L.tnt[t][1] * L.tnt[t][2] : 0;
+  }
   size_t o = 0;
   L.ctr = o;
   o += al(sizeof(Counters));
@@ -113,6 +137,10 @@ CLayout compress_layout(const Shape& s, bool host_in, bool host_out) {
   o += al(2 * 4 * L.bmw);
   L.state = o;
   o += al(8 * (s.C / kScanTile + 1));
+  L.act0 = o;
+  o += al(4 * L.tn[0]);
+  L.act1 = o;
+  o += al(4 * L.tn[1]);
   L.zero_end = o;
   L.plist = o;
   o += al(2 * (s.n < (1ull << 31) - (1ull << 24) ? 4 : 8) * s.n);
@@ -121,6 +149,12 @@ CLayout compress_layout(const Shape& s, bool host_in, bool host_out) {
   o += al(4ull * s.d0 * s.d1 * L.nseg * (s.ndims == 3 ? Geo<3>::SW : Geo<2>::SW));
   L.s = o;
   o += al(4 * s.n);
+  L.sp = o;  // subbin planes (k_tiles): 8 words per 32-point segment
+  o += al(4ull * kSP * s.d0 * s.d1 * L.nseg);
+  L.list0 = o;
+  o += al(4 * L.tn[0]);
+  L.list1 = o;
+  o += al(4 * L.tn[1]);
   L.stage = o;
   o += al(2ull * kChunkBytes * s.C);
   L.sizes = o;
@@ -150,15 +184,19 @@ struct DevInfo {
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   cudaStream_t side2 = nullptr;            // host-I/O decompress: D2H of decoded ranges
   cudaEvent_t ev_in[4] = {}, ev_dec[4] = {}, ev_out = nullptr;
-  int occ_sweep2 = 0, occ_sweep3 = 0, occ_sweep2w = 0, occ_sweep3w = 0, occ_decode = 0;
+  int occ_sweep2 = 0, occ_sweep3 = 0, occ_sweep2w = 0, occ_sweep3w = 0, occ_decode = 0, occ_tiles2 = 0, occ_tiles3 = 0;
   bool attrs = false;
 };
-DevInfo g_dev;
+// One per (host thread, device): created on the thread's first call on that
+// device, never re-created (no leak on device switches).
+thread_local DevInfo tl_dev[kMaxDev];
 
 int dev_info(DevInfo*& out) {
   int dev;
   CK(cudaGetDevice(&dev));
-  if (g_dev.dev != dev || !g_dev.attrs) {
+  if (dev < 0 || dev >= kMaxDev) return LOPC_E_ARG;
+  DevInfo& g_dev = tl_dev[dev];
+  if (!g_dev.attrs) {
     g_dev = DevInfo{};
     g_dev.dev = dev;
     CK(cudaStreamCreateWithFlags(&g_dev.side, cudaStreamNonBlocking));
@@ -192,6 +230,8 @@ int dev_info(DevInfo*& out) {
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_dev.occ_sweep3, k_sweep<3, int32_t>, kSweepThreads, 0));
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_dev.occ_sweep2w, k_sweep<2, int64_t>, kSweepThreads, 0));
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_dev.occ_sweep3w, k_sweep<3, int64_t>, kSweepThreads, 0));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_dev.occ_tiles2, k_tiles<2>, kTileThreads, 0));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_dev.occ_tiles3, k_tiles<3>, kTileThreads, 0));
     {
       cudaLaunchConfig_t cfg{};
       cfg.gridDim = dim3(2 * 148 * 8, 1, 1);
@@ -205,20 +245,21 @@ int dev_info(DevInfo*& out) {
   return LOPC_OK;
 }
 
-// pinned status block for the single D2H read per call
-Counters* g_host_ctr = nullptr;
+// Pinned status slot for the single D2H read per call: one per host thread
+// (a call blocks its thread until the slot has been read, so calls of
+// different threads never share one).
+thread_local Counters* tl_host_ctr = nullptr;
 int host_ctr(Counters*& h) {
-  if (!g_host_ctr) CK(cudaMallocHost(&g_host_ctr, sizeof(Counters)));
-  h = g_host_ctr;
+  if (!tl_host_ctr) CK(cudaMallocHost(&tl_host_ctr, sizeof(Counters)));
+  h = tl_host_ctr;
   return LOPC_OK;
 }
 
 // Per-call CUDA-event marks (lopc_set_timing).  The events are created once
-// per device and reused, so timing adds no allocation to the call.
-cudaEvent_t g_ev[8] = {};
-int g_ev_dev = -1;
+// per (thread, device) and reused, so timing adds no allocation to the call.
+thread_local cudaEvent_t g_ev_all[kMaxDev][8] = {};
 struct Timer {
-  cudaEvent_t* ev = g_ev;
+  cudaEvent_t* ev = nullptr;
   int n = 0;
   bool on = false;
   cudaStream_t st = nullptr;
@@ -228,10 +269,10 @@ struct Timer {
     if (!on) return LOPC_OK;
     int dev;
     CK(cudaGetDevice(&dev));
-    if (g_ev_dev != dev) {
-      for (int i = 0; i < 8; ++i) CK(cudaEventCreate(&g_ev[i]));
-      g_ev_dev = dev;
-    }
+    if (dev < 0 || dev >= kMaxDev) return LOPC_E_ARG;
+    ev = g_ev_all[dev];
+    if (!ev[0])
+      for (int i = 0; i < 8; ++i) CK(cudaEventCreate(&ev[i]));
     return LOPC_OK;
   }
   void mark() {
@@ -296,7 +337,7 @@ RepairArgs make_repair_args(const Shape& sh, const void* x, double eps, uint8_t*
   ra.own_hi = (int64_t)sh.n;
   ra.skip_dense = 0;
   ra.prof = g_timing >= 2;
-  ra.engine = g_engine;
+  ra.engine = 0;
   return ra;
 }
 
@@ -309,14 +350,11 @@ typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t,
                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 EncodeTiledFn g_encode_tiled = nullptr;
-bool g_encode_tried = false;
+std::once_flag g_encode_once;
 int g_use_tma = 1;  // LOPC_NO_TMA=1 in the environment disables (tests cover both paths)
 
 bool make_halo_map(const Shape& sh, const void* x, CUtensorMap* m) {
-  if (!g_use_tma || (uintptr_t)x % 16 || (sh.d2 * sh.k) % 16) return false;
-  if (sh.d0 > (1ull << 31) || sh.d1 > (1ull << 31) || sh.d2 > (1ull << 31)) return false;
-  if (!g_encode_tried) {
-    g_encode_tried = true;
+  std::call_once(g_encode_once, [] {
     const char* env = getenv("LOPC_NO_TMA");
     if (env && env[0] == '1') g_use_tma = 0;
     void* fn = nullptr;
@@ -324,8 +362,9 @@ bool make_halo_map(const Shape& sh, const void* x, CUtensorMap* m) {
     if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
         q == cudaDriverEntryPointSuccess)
       g_encode_tiled = reinterpret_cast<EncodeTiledFn>(fn);
-    if (!g_use_tma) return false;
-  }
+  });
+  if (!g_use_tma || (uintptr_t)x % 16 || (sh.d2 * sh.k) % 16) return false;
+  if (sh.d0 > (1ull << 31) || sh.d1 > (1ull << 31) || sh.d2 > (1ull << 31)) return false;
   if (!g_encode_tiled) return false;
   const CUtensorMapDataType dt = sh.k == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64;
   CUresult r;
@@ -397,39 +436,97 @@ int launch_sweep(const Shape& sh, RepairArgs& ra, const CLayout& L, cudaStream_t
   return LOPC_OK;
 }
 
+// a3 on the tile engine: one cooperative k_tiles launch (tile fixpoints over
+// alternating shifted tilings, subbin planes), then the planes widened to one
+// u32 per point for the encoder.
+int launch_tiles(const Shape& sh, const RepairArgs& ra, uint8_t* ws, const CLayout& L, cudaStream_t st) {
+  DevInfo* di;
+  int rc = dev_info(di);
+  if (rc) return rc;
+  TileArgs ta{};
+  ta.flags = ra.flags;
+  ta.sp = reinterpret_cast<uint32_t*>(ws + L.sp);
+  ta.act[0] = reinterpret_cast<uint32_t*>(ws + L.act0);
+  ta.act[1] = reinterpret_cast<uint32_t*>(ws + L.act1);
+  ta.list[0] = reinterpret_cast<uint32_t*>(ws + L.list0);
+  ta.list[1] = reinterpret_cast<uint32_t*>(ws + L.list1);
+  ta.ctr = ra.ctr;
+  ta.d0 = (int64_t)sh.d0;
+  ta.d1 = (int64_t)sh.d1;
+  ta.d2 = (int64_t)sh.d2;
+  ta.nseg = (int64_t)L.nseg;
+  memcpy(ta.nt, L.tnt, sizeof(ta.nt));
+  ta.ntiles[0] = (uint32_t)L.tn[0];
+  ta.ntiles[1] = (uint32_t)L.tn[1];
+  ta.max_passes = 1 << 20;
+  ta.prof = g_timing >= 2;
+  const int occ = sh.ndims == 3 ? di->occ_tiles3 : di->occ_tiles2;
+  uint64_t grid = (uint64_t)occ * di->sms;
+  const uint64_t need = (L.tn[1] + kTileWarps - 1) / kTileWarps;
+  if (grid > need) grid = need;
+  if (grid < 1) grid = 1;
+  void* kargs[] = {&ta};
+  if (sh.ndims == 3)
+    CK(cudaLaunchCooperativeKernel((void*)k_tiles<3>, dim3((unsigned)grid), dim3(kTileThreads), kargs, 0, st));
+  else
+    CK(cudaLaunchCooperativeKernel((void*)k_tiles<2>, dim3((unsigned)grid), dim3(kTileThreads), kargs, 0, st));
+  uint64_t g2 = (sh.d0 * sh.d1 * L.nseg * 32 + 255) / 256;
+  if (g2 > (uint64_t)di->sms * 16) g2 = (uint64_t)di->sms * 16;
+  if (sh.ndims == 3)
+    k_planes_to_s<3><<<(unsigned)g2, 256, 0, st>>>(ta.sp, ra.s, ta.d0, ta.d1, ta.d2, ta.nseg);
+  else
+    k_planes_to_s<2><<<(unsigned)g2, 256, 0, st>>>(ta.sp, ra.s, ta.d0, ta.d1, ta.d2, ta.nseg);
+  CK(cudaGetLastError());
+  return LOPC_OK;
+}
+
+// Repair engines: 0 = tile fixpoints (default; lopc_tiles.cuh), 1 = the
+// paper's point worklist (f2), 2 = r1's dense tile pass + point worklist
+// (k_sweep, u32 subbins; also the fallback when a subbin exceeds 8 planes).
+enum { kEngTiles = 0, kEngPaper = 1, kEngSweep = 2 };
+constexpr int kRetryU32 = 1;  // internal: re-run the repair on kEngSweep
+
 // Steps a1-a3 (quantize, flags, repair to the fixpoint) on device input.
 int run_repair(const Shape& sh, const void* x, double eps, uint8_t* ws, const CLayout& L, cudaStream_t st, Timer& tm,
-               Counters* hc) {
+               int engine) {
   RepairArgs ra = make_repair_args(sh, x, eps, ws, L);
+  ra.engine = engine == kEngPaper ? 1 : 0;
   int rc = launch_quant_flags(sh, ra, L, st);
   if (rc) return rc;
   if (ra.engine) CK(cudaMemsetAsync(ra.s, 0, 4 * sh.n, st));  // the worklist engine starts from s = 0
   tm.mark();
-  if ((rc = launch_sweep(sh, ra, L, st))) return rc;
+  if (engine == kEngTiles)
+    rc = launch_tiles(sh, ra, ws, L, st);
+  else
+    rc = launch_sweep(sh, ra, L, st);
+  if (rc) return rc;
   tm.mark();
-  (void)hc;
   return LOPC_OK;
 }
 
+// Workspace of the plain calls: one pool per (host thread, device), grown on
+// demand.  The plain calls run on the legacy default stream and block until
+// done, so a thread's pool is never in use by two calls at once.
+thread_local void* tl_pool[kMaxDev] = {};
+thread_local size_t tl_pool_size[kMaxDev] = {};
 int workspace_for(size_t need, void*& ws, size_t& ws_bytes) {
-  static void* pool = nullptr;
-  static size_t pool_size = 0;
-  static int pool_dev = -1;
   int dev;
   CK(cudaGetDevice(&dev));
-  if (pool && (pool_size < need || pool_dev != dev)) {
+  if (dev < 0 || dev >= kMaxDev) return LOPC_E_ARG;
+  void*& pool = tl_pool[dev];
+  if (pool && tl_pool_size[dev] < need) {
+    CK(cudaDeviceSynchronize());  // the legacy stream's last use of the old pool
     cudaFree(pool);
     pool = nullptr;
-    pool_size = 0;
+    tl_pool_size[dev] = 0;
   }
   if (!pool) {
     size_t sz = need < (1u << 20) ? (1u << 20) : need;
     CK(cudaMalloc(&pool, sz));
-    pool_size = sz;
-    pool_dev = dev;
+    tl_pool_size[dev] = sz;
   }
   ws = pool;
-  ws_bytes = pool_size;
+  ws_bytes = tl_pool_size[dev];
   return LOPC_OK;
 }
 
@@ -459,7 +556,7 @@ const char* lopc_last_error_string(void) { return g_errmsg; }
 void lopc_set_timing(int enable) { g_timing = enable; }
 
 int lopc_set_repair_engine(int engine) {
-  if (engine != 0 && engine != 1) return LOPC_E_ARG;
+  if (engine < 0 || engine > 2) return LOPC_E_ARG;
   g_engine = engine;
   return LOPC_OK;
 }
@@ -517,8 +614,11 @@ int lopc_stream_info(const void* host_hdr, size_t n, int* ndims, uint64_t* dims3
   return LOPC_OK;
 }
 
-int lopc_compress_ex(const void* in, int ndims, const uint64_t* dims, int dtype, double eps, void* out,
-                     size_t* out_bytes, void* workspace, size_t workspace_bytes, void* stream) {
+}  // extern "C"
+
+namespace {
+int compress_impl(const void* in, int ndims, const uint64_t* dims, int dtype, double eps, void* out,
+                  size_t* out_bytes, void* workspace, size_t workspace_bytes, void* stream, int engine) {
   if (!out_bytes) return LOPC_E_ARG;
   Shape sh;
   int rc = make_shape(ndims, dims, dtype, sh);
@@ -604,7 +704,7 @@ int lopc_compress_ex(const void* in, int ndims, const uint64_t* dims, int dtype,
     CK(cudaGetLastError());
     CK(cudaEventRecord(di->ev_join, di->side));
   }
-  if ((rc = run_repair(sh, x, eps, ws, L, st, tm, hc))) return rc;  // marks 3, 4
+  if ((rc = run_repair(sh, x, eps, ws, L, st, tm, engine))) return rc;  // marks 3, 4
   if (!overlap && !(!tm.on && ovl_mode == 2)) launch_encode(ea, sh.dtype == LOPC_F64, 1, (unsigned)sh.C, smem, st);
   launch_encode(ea, sh.dtype == LOPC_F64, 2, (unsigned)sh.C, smem, st);
   CK(cudaGetLastError());
@@ -662,7 +762,10 @@ int lopc_compress_ex(const void* in, int ndims, const uint64_t* dims, int dtype,
   if (g_timing >= 2)  // diagnostic: dense-pass cycles per phase (levels, s write, border) in phase_cycles[5..7]
     for (int i = 1; i < 4; ++i) g_stats.phase_cycles[4 + i] += hc->dense_cycles[i];
   uint32_t err = hc->err;
-  if (hc->passes >= (unsigned long long)(1 << 20) && hc->list_count[(hc->passes + 1) % 3] != 0) err |= kErrPassCap;
+  if (err & kErrPlanes) return kRetryU32;  // a subbin above 8 planes: the caller re-runs on the u32 engine
+  if (hc->passes >= (unsigned long long)(1 << 20) &&
+      (engine == kEngTiles ? hc->tl_count[(hc->passes + 1) % 3] : hc->list_count[(hc->passes + 1) % 3]) != 0)
+    err |= kErrPassCap;
   if ((rc = map_err(err & ~kErrNoSpace))) return rc;
   if (total > cap) {
     *out_bytes = total;
@@ -686,6 +789,21 @@ int lopc_compress_ex(const void* in, int ndims, const uint64_t* dims, int dtype,
     g_stats.ms_total = tm.ms(0, 7);
   }
   return LOPC_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int lopc_compress_ex(const void* in, int ndims, const uint64_t* dims, int dtype, double eps, void* out,
+                     size_t* out_bytes, void* workspace, size_t workspace_bytes, void* stream) {
+  const size_t cap = out_bytes ? *out_bytes : 0;
+  int rc = compress_impl(in, ndims, dims, dtype, eps, out, out_bytes, workspace, workspace_bytes, stream, g_engine);
+  if (rc == kRetryU32) {  // the tile engine's 8 subbin planes overflowed: the u32 engine, same result
+    *out_bytes = cap;
+    rc = compress_impl(in, ndims, dims, dtype, eps, out, out_bytes, workspace, workspace_bytes, stream, kEngSweep);
+  }
+  return rc;
 }
 
 int lopc_compress(const void* in, int ndims, const uint64_t* dims, int dtype, double eps, void* out,
@@ -720,8 +838,14 @@ int lopc_repair_ex(const void* in, int ndims, const uint64_t* dims, int dtype, d
   Counters* hc;
   if ((rc = host_ctr(hc))) return rc;
   Timer tm;
-  CK(cudaMemsetAsync(ws, 0, L.zero_end, st));
-  if ((rc = run_repair(sh, in, eps, ws, L, st, tm, hc))) return rc;
+  for (int engine = g_engine;;) {
+    CK(cudaMemsetAsync(ws, 0, L.zero_end, st));
+    if ((rc = run_repair(sh, in, eps, ws, L, st, tm, engine))) return rc;
+    CK(cudaMemcpyAsync(hc, ws + L.ctr, sizeof(Counters), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (!(hc->err & kErrPlanes)) break;
+    engine = kEngSweep;  // a subbin above 8 planes: the u32 engine
+  }
   if (subbins_out) CK(cudaMemcpyAsync(subbins_out, ws + L.s, 4 * sh.n, cudaMemcpyDeviceToDevice, st));
   if (flags_out) {
     const uint32_t* fw = reinterpret_cast<const uint32_t*>(ws + L.flags);
@@ -731,7 +855,6 @@ int lopc_repair_ex(const void* in, int ndims, const uint64_t* dims, int dtype, d
       k_unpack_flags<2><<<1024, 256, 0, st>>>(fw, flags_out, sh.d0, sh.d1, sh.d2, (int64_t)L.nseg);
     CK(cudaGetLastError());
   }
-  CK(cudaMemcpyAsync(hc, ws + L.ctr, sizeof(Counters), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   g_stats = lopc_stats{};
   g_stats.n_elems = sh.n;

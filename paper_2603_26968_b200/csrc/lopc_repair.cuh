@@ -149,6 +149,8 @@ struct Counters {
   unsigned long long ghost_changed;  // slab mode: ghosts raised by the last k_ghost_inject
   unsigned long long pass_ns[kPassHist];  // diagnostic (prof): k_sweep pass end times, ns after the launch
   unsigned long long dense_cycles[4];     // diagnostic (prof): dense pass load / levels / s write / border, per warp
+  uint32_t tl_count[3];   // k_tiles: active-tile list lengths (rotating by pass)
+  uint32_t tl_ticket[3];  // k_tiles: per-pass tile tickets (rotating)
 };
 
 // Diagnostic phase clock: thread 0 of a block adds the cycles since the last
@@ -176,6 +178,7 @@ enum : uint32_t {
   kErrOverflow = 8u,
   kErrPassCap = 16u,
   kErrVersion = 32u,
+  kErrPlanes = 64u,  // k_tiles: a subbin above kMaxPlaneLevel (the host reruns with the u32 engine)
 };
 
 struct RepairArgs {

@@ -8,6 +8,7 @@ missing or no GPU is visible, every call raises.
 from __future__ import annotations
 
 import ctypes as C
+import threading
 import os
 import re
 
@@ -142,15 +143,18 @@ def _check(rc: int, what: str):
         raise LopcError(rc, what, load(False).lopc_last_error_string().decode())
 
 
-_ws = {}
+_ws = threading.local()  # one workspace per (host thread, device): calls of two threads never share one
 
 
 def _workspace(nbytes: int, device) -> torch.Tensor:
     key = torch.device(device).index if torch.device(device).type == "cuda" else torch.cuda.current_device()
-    t = _ws.get(key)
+    d = getattr(_ws, "d", None)
+    if d is None:
+        d = _ws.d = {}
+    t = d.get(key)
     if t is None or t.numel() < nbytes:
         t = torch.empty(max(nbytes, 1 << 20), dtype=torch.uint8, device=f"cuda:{key}")
-        _ws[key] = t
+        d[key] = t
     return t
 
 
@@ -243,7 +247,9 @@ def set_timing(on=True):
 
 
 def set_repair_engine(engine: int):
-    """0: dense tile levels + worklist tail (default); 1: the paper's point worklist."""
+    """0: tile fixpoints over alternating shifted tilings (default; falls back
+    to 2 when a subbin exceeds 8 planes); 1: the paper's point worklist (f2);
+    2: r1's dense tile pass + point worklist tail (u32 subbins)."""
     L = load(False)
     L.lopc_set_repair_engine.argtypes = [C.c_int]
     L.lopc_set_repair_engine.restype = C.c_int
