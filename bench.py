@@ -591,7 +591,10 @@ def main():
     med = {kk: statistics.median(v) for kk, v in kern.items()}
     alg = {
         "quant_flags": n * (k + F),                                        # read x, write flags
-        "sweep": n * (F + 4) + statistics.median(tiles) * (F + 4),         # dense: flags -> s; sparse: per point
+        # tile engine (k_tiles): pass 1 reads the flags and writes the subbin
+        # planes (F + 1 B/point); every later tile visit (1024 points) reads
+        # flags + planes and writes planes (F + 2 B/point)
+        "sweep": n * (F + 1) + max(0, statistics.median(tiles) - rep["pass_items"][0]) * 1024 * (F + 2),
         "encode": n * (k + 4) + nbytes_stream,                             # read x + s, write payloads
         "place": 2 * nbytes_stream,                                        # staged payloads -> stream
         "decode_scan": 16 * ((n * k + 16383) // 16384),                   # size table in, offsets out

@@ -22,7 +22,15 @@
  *    calls use a grow-only internal workspace on the current device and the
  *    legacy default stream.  No allocation happens inside *_ex.
  *  - Every call blocks until its result code is known (one device->host read
- *    of an 8..256-byte status block at the end).
+ *    of the status block at the end, into a pinned slot owned by the calling
+ *    host thread).
+ *  - Concurrency: calls on different streams with different
+ *    workspaces are independent and may run at the same time from different
+ *    host threads.  Everything a call writes on the host side is per thread
+ *    (status slot, lopc_last_stats, lopc_last_error_string, the side streams
+ *    and events of the host-I/O decompress pipeline, the plain calls'
+ *    workspace pool), keyed by device.  lopc_set_timing and
+ *    lopc_set_repair_engine are process-wide settings.
  *  - Return value: LOPC_OK (0) or a negative LOPC_E_* code.  On LOPC_E_NOSPACE
  *    from a compress call, *out_bytes holds the size required.  Output buffer
  *    contents are unspecified on error.
@@ -52,11 +60,12 @@ enum {
   LOPC_E_CORRUPT = -4,  /* malformed stream (header, size table or payload) */
   LOPC_E_VERSION = -5,  /* stream version != 1 */
   LOPC_E_CUDA = -6,     /* CUDA runtime error (message: lopc_last_error_string) */
-  LOPC_E_NCCL = -7,     /* reserved for the multi-GPU slab mode */
+  LOPC_E_NCCL = -7,     /* NCCL failure in the multi-GPU slab mode */
   LOPC_E_INTERNAL = -8  /* a self-check failed (bound re-check a4, subbin overflow, pass cap) */
 };
 
-/* Worst-case stream size: 64 + 8C + 2 * 16384 * C bytes, C = ceil(N / (16384/k)). */
+/* Worst-case stream size: 64 + 8C + 2 * 16384 * C bytes, C = ceil(N / (16384/k))
+ * (16 kB chunks; raw fallback per payload, reading G23). */
 size_t lopc_compress_bound(int ndims, const uint64_t* dims, int dtype);
 
 /* Workspace bytes for lopc_compress_ex.  host_io != 0 adds room to stage a
@@ -68,39 +77,54 @@ size_t lopc_compress_workspace_bytes(int ndims, const uint64_t* dims, int dtype,
 size_t lopc_decompress_workspace_bytes(size_t in_bytes, size_t out_bytes, int host_io);
 
 /* Compress x (N values of dtype) with absolute error bound eps (ABS; for NOA
- * the caller passes eps = rel * (max - min)).  *out_bytes: in = the
- * capacity of out, out = bytes written (or required, on LOPC_E_NOSPACE). */
+ * the caller passes eps = rel * (max - min)): quantization to bins
+ * b = floor(x/eps + 1/2) with the exact double-check (§IV.A, G6-G9),
+ * flags and the repair of the subbins to the least fixpoint (§IV.B, Alg. 1
+ * P:127-154, Alg. 2; "as low as possible"), the bound
+ * self-check a4, and the chunk pipelines DIFF-NB-BIT-RZE (bins,
+ * P:90-91) and BIT-RZE_k-RZE_1 (subbins) placed by one
+ * prefix sum.  Stream format: DESIGN.md §4.  *out_bytes: in = the
+ * capacity of out, out = bytes written (or required, on LOPC_E_NOSPACE).
+ * Errors: E_ARG (null in/out/out_bytes, eps outside [2^-900, 2^1000]),
+ * E_SHAPE, E_NOSPACE (out or workspace too small), E_CUDA, E_INTERNAL. */
 int lopc_compress(const void* in, int ndims, const uint64_t* dims, int dtype, double eps, void* out,
                   size_t* out_bytes);
 int lopc_compress_ex(const void* in, int ndims, const uint64_t* dims, int dtype, double eps, void* out,
                      size_t* out_bytes, void* workspace, size_t workspace_bytes, void* stream);
 
 /* Decompress a stream of in_bytes bytes into out (capacity out_capacity
- * bytes, must hold N*k).  The header is validated on the device; corrupt
- * streams return LOPC_E_CORRUPT without partial-output guarantees. */
+ * bytes, must hold N*k): the inverse chunk pipelines, then per point the
+ * value whose key is key(lo(b)) + s ("subbin 0 decodes to the lowest
+ * representable value within the bin"; escapes bit-exact, G10); the
+ * decoder is "embarrassingly parallel".  The header and size table
+ * are validated before any payload is read; corrupt streams return
+ * LOPC_E_CORRUPT (LOPC_E_VERSION for a version != 1) without
+ * partial-output guarantees; E_NOSPACE if out_capacity < N*k. */
 int lopc_decompress(const void* in, size_t in_bytes, void* out, size_t out_capacity);
 int lopc_decompress_ex(const void* in, size_t in_bytes, void* out, size_t out_capacity, void* workspace,
                        size_t workspace_bytes, void* stream);
 
-/* Host-side parse of a stream header (host pointer, >= 64 bytes).  dims3 gets
- * (d0, d1, d2) with d0 = 1 for 2D.  Any output pointer may be NULL. */
+/* Host-side parse of a stream header (host pointer, >= 64
+ * bytes).  dims3 gets (d0, d1, d2) with d0 = 1 for 2D.  Any output pointer
+ * may be NULL.  E_CORRUPT for a short or malformed header, E_VERSION. */
 int lopc_stream_info(const void* host_hdr, size_t n, int* ndims, uint64_t* dims3, int* dtype, double* eps,
                      uint64_t* n_elems, uint32_t* n_chunks);
 
-/* Parity/diagnostic hook: run steps a1-a3 only and copy the flags (as u16,
- * Alg. 1 loop 2, slot order G2) and the final subbins (u32) into the given
- * device buffers (N entries each; either may be NULL).  Uses the
+/* Parity/diagnostic hook: run steps a1-a3 only (Alg. 1 P:137-146,
+ * Alg. 2) and copy the flags (as u16, Alg. 1 loop 2, slot order
+ * G2) and the final subbins (u32) into the given device buffers (N entries
+ * each; either may be NULL).  Device input only (E_ARG otherwise).  Uses the
  * lopc_compress_ex workspace. */
 int lopc_repair_ex(const void* in, int ndims, const uint64_t* dims, int dtype, double eps, uint16_t* flags_out,
                    uint32_t* subbins_out, void* workspace, size_t workspace_bytes, void* stream);
 
-/* Statistics of the last compress/decompress call on this process. */
+/* Statistics of the calling host thread's last compress/decompress call. */
 typedef struct {
   uint64_t n_elems;
   uint64_t n_chunks;
   uint64_t n_tiles;
-  uint64_t sweep_passes;      /* k_sweep passes: 1 dense tile pass + sparse point-worklist passes */
-  uint64_t worklist_points;   /* sum of worklist points over the sparse passes */
+  uint64_t sweep_passes;      /* repair passes (engine 0: tile passes of k_tiles; 1/2: k_sweep passes) */
+  uint64_t worklist_points;   /* engine 0: tiles processed over all passes; 1/2: worklist points */
   uint64_t inner_iters;       /* sum of tile-local relaxation rounds in the dense pass */
   uint64_t escapes;
   uint64_t bin_bytes;
@@ -115,8 +139,8 @@ typedef struct {
   float ms_decode;            /* k_decode */
   float ms_d2h;               /* device->host staging */
   float ms_total;             /* whole call on the stream */
-  uint64_t raised;            /* subbins raised above 0 (dense pass) or raised again (sparse passes) */
-  uint32_t pass_items[16];    /* [1]: tiles of the dense pass; [q>1]: worklist points of pass q */
+  uint64_t raised;            /* engine 0: subbins changed, summed over passes; 1/2: raises */
+  uint32_t pass_items[16];    /* engine 0: tiles of pass q at [q]; 1/2: [1] dense tiles, [q>1] worklist points */
   uint64_t phase_cycles[16];  /* diagnostic (lopc_set_timing(2)): SM cycles per codec phase, summed over chunks */
   float ms_place;             /* compress: k_chunk_scan + k_place; decompress: k_chunk_scan */
   uint32_t launches;          /* kernels this library launched in the call */
@@ -130,14 +154,18 @@ int lopc_last_stats(lopc_stats* out);
  * records per-phase clocks of the codec kernels (diagnostic, slower). */
 void lopc_set_timing(int enable);
 
-/* Repair schedule (process-wide; NEXT f2 ablation).  0 (default): a dense,
- * exact tile-local level-set pass then point worklist passes for what crosses
- * tiles; 1: the paper's point worklist from the first pass (Alg. 2 over every
- * point, then the points whose inputs rose).  Both reach the same
- * unique least fixpoint, hence the same bytes.  Slab mode uses engine 0. */
+/* Repair schedule (process-wide; NEXT f2 ablation).  0 (default): exact
+ * tile fixpoints over alternating half-shifted tilings with subbin bit planes
+ * (lopc_tiles.cuh), falling back to 2 when a subbin exceeds 254; 1: the
+ * paper's point worklist from the first pass (Alg. 2 over every point, then
+ * the points whose inputs rose); 2: round 1's dense tile pass
+ * then point-worklist passes (u32 subbins).  All reach the same unique least
+ * fixpoint (reading G14), hence the same bytes.  Slab mode uses engine 2.
+ * E_ARG for another value. */
 int lopc_set_repair_engine(int engine);
 
-/* Message for a return code; lopc_last_error_string() adds CUDA detail. */
+/* Message for a return code; lopc_last_error_string() adds CUDA / NCCL
+ * detail of the calling thread's last failure. */
 const char* lopc_strerror(int code);
 const char* lopc_last_error_string(void);
 
@@ -210,8 +238,14 @@ int lopc_compress_noa(const void* in, int ndims, const uint64_t* dims, int dtype
  *   header(total) ‖ table slices in rank order ‖ payload slices in rank order,
  * and *payload_offset is where this rank's payload slice starts in it.
  * Device pointers only (in_slab, out_local, workspace).  Errors are agreed
- * across ranks (every rank returns the worst code).  A NULL comm means
- * world = 1.
+ * across ranks (every rank returns the worst code): at entry (an allgather of
+ * the ranges and local checks), after every repair round (the round's
+ * allreduce carries a failure count, so a rank that fails locally keeps
+ * taking part in the collectives and all ranks stop together) and at exit
+ * (an allgather of sizes and codes).  A failing NCCL call itself returns
+ * LOPC_E_NCCL at once; the communicator is then unusable.  A NULL comm means
+ * world = 1.  SURVEY §8(e); the exchange is the one of Alg. 2's sweeps
+ * across slab boundaries.
  */
 typedef struct lopc_comm lopc_comm;
 

@@ -118,10 +118,10 @@ CLayout compress_layout(const Shape& s, bool host_in, bool host_out) {
   }
   L.ntiles = s.n ? (uint64_t)L.ntz * L.nty * L.ntx : 0;
   {
-    using B3 = TBox<3>;
-    using B2 = TBox<2>;
-    const uint64_t TZ = s.ndims == 3 ? Geo<3>::TZ : 1, TY = s.ndims == 3 ? Geo<3>::TY : Geo<2>::TY;
-    const uint64_t SZ = s.ndims == 3 ? B3::SZ : 0, SY = s.ndims == 3 ? B3::SY : B2::SY;
+    using T3 = TG<3>;
+    using T2 = TG<2>;
+    const uint64_t TZ = s.ndims == 3 ? T3::TZ : 1, TY = s.ndims == 3 ? T3::TY : T2::TY;
+    const uint64_t SZ = s.ndims == 3 ? T3::SZ : 0, SY = s.ndims == 3 ? T3::SY : T2::SY;
     L.tnt[0][0] = (uint32_t)((s.d0 + TZ - 1) / TZ);
     L.tnt[0][1] = (uint32_t)((s.d1 + TY - 1) / TY);
     L.tnt[1][0] = (uint32_t)((s.d0 + SZ + TZ - 1) / TZ);
@@ -439,7 +439,7 @@ int launch_sweep(const Shape& sh, RepairArgs& ra, const CLayout& L, cudaStream_t
 // a3 on the tile engine: one cooperative k_tiles launch (tile fixpoints over
 // alternating shifted tilings, subbin planes), then the planes widened to one
 // u32 per point for the encoder.
-int launch_tiles(const Shape& sh, const RepairArgs& ra, uint8_t* ws, const CLayout& L, cudaStream_t st) {
+int launch_tiles(const Shape& sh, const RepairArgs& ra, uint8_t* ws, const CLayout& L, cudaStream_t st, bool widen) {
   DevInfo* di;
   int rc = dev_info(di);
   if (rc) return rc;
@@ -470,6 +470,8 @@ int launch_tiles(const Shape& sh, const RepairArgs& ra, uint8_t* ws, const CLayo
     CK(cudaLaunchCooperativeKernel((void*)k_tiles<3>, dim3((unsigned)grid), dim3(kTileThreads), kargs, 0, st));
   else
     CK(cudaLaunchCooperativeKernel((void*)k_tiles<2>, dim3((unsigned)grid), dim3(kTileThreads), kargs, 0, st));
+  CK(cudaGetLastError());
+  if (!widen) return LOPC_OK;  // compress: the encoder reads the planes
   uint64_t g2 = (sh.d0 * sh.d1 * L.nseg * 32 + 255) / 256;
   if (g2 > (uint64_t)di->sms * 16) g2 = (uint64_t)di->sms * 16;
   if (sh.ndims == 3)
@@ -488,7 +490,7 @@ constexpr int kRetryU32 = 1;  // internal: re-run the repair on kEngSweep
 
 // Steps a1-a3 (quantize, flags, repair to the fixpoint) on device input.
 int run_repair(const Shape& sh, const void* x, double eps, uint8_t* ws, const CLayout& L, cudaStream_t st, Timer& tm,
-               int engine) {
+               int engine, bool widen) {
   RepairArgs ra = make_repair_args(sh, x, eps, ws, L);
   ra.engine = engine == kEngPaper ? 1 : 0;
   int rc = launch_quant_flags(sh, ra, L, st);
@@ -496,7 +498,7 @@ int run_repair(const Shape& sh, const void* x, double eps, uint8_t* ws, const CL
   if (ra.engine) CK(cudaMemsetAsync(ra.s, 0, 4 * sh.n, st));  // the worklist engine starts from s = 0
   tm.mark();
   if (engine == kEngTiles)
-    rc = launch_tiles(sh, ra, ws, L, st);
+    rc = launch_tiles(sh, ra, ws, L, st, widen);
   else
     rc = launch_sweep(sh, ra, L, st);
   if (rc) return rc;
@@ -689,26 +691,21 @@ int compress_impl(const void* in, int ndims, const uint64_t* dims, int dtype, do
   ea.d2 = sh.d2;
   set_escape_limits(ea, sh.dtype == LOPC_F64, eps);
   const size_t smem = sizeof(EncSmem);
-  // Stream order: repair, bin-stream encode, subbin-stream encode.
-  // LOPC_OVERLAP=1 runs the bin-stream encode on a side stream beside the
-  // repair (it only depends on x), =2 before it; measured on cfg2 (r1f) both
-  // are slower than the default serial order (0.665 / 0.656 vs 0.651 ms): the
-  // repair leaves no room on the SMs (k_sweep fills the register file).
-  static const int ovl_mode = getenv("LOPC_OVERLAP") ? atoi(getenv("LOPC_OVERLAP")) : 0;
-  const bool overlap = !tm.on && ovl_mode == 1;
-  if (!tm.on && ovl_mode == 2) launch_encode(ea, sh.dtype == LOPC_F64, 1, (unsigned)sh.C, smem, st);
-  if (overlap) {
-    CK(cudaEventRecord(di->ev_fork, st));
-    CK(cudaStreamWaitEvent(di->side, di->ev_fork, 0));
-    launch_encode(ea, sh.dtype == LOPC_F64, 1, (unsigned)sh.C, smem, di->side);
-    CK(cudaGetLastError());
-    CK(cudaEventRecord(di->ev_join, di->side));
+  // Stream order: repair, bin-stream encode, subbin-stream encode.  (r1
+  // measured the bin encode beside the repair on a side stream: slower, the
+  // repair fills the SMs; with subbin planes the bin CTAs also run a4, which
+  // needs the repaired subbins.)
+  if ((rc = run_repair(sh, x, eps, ws, L, st, tm, engine, false))) return rc;  // marks 3, 4
+  if (engine == kEngTiles) {  // the encoder reads the subbin planes and the flags' escape words
+    ea.sp = reinterpret_cast<const uint32_t*>(ws + L.sp);
+    ea.flags = reinterpret_cast<const uint32_t*>(ws + L.flags);
+    ea.nseg = (int64_t)L.nseg;
+    ea.sw = sh.ndims == 3 ? Geo<3>::SW : Geo<2>::SW;
+    ea.esc_word = ea.sw - 2;
   }
-  if ((rc = run_repair(sh, x, eps, ws, L, st, tm, engine))) return rc;  // marks 3, 4
-  if (!overlap && !(!tm.on && ovl_mode == 2)) launch_encode(ea, sh.dtype == LOPC_F64, 1, (unsigned)sh.C, smem, st);
+  launch_encode(ea, sh.dtype == LOPC_F64, 1, (unsigned)sh.C, smem, st);
   launch_encode(ea, sh.dtype == LOPC_F64, 2, (unsigned)sh.C, smem, st);
   CK(cudaGetLastError());
-  if (overlap) CK(cudaStreamWaitEvent(st, di->ev_join, 0));
   tm.mark();  // 5
   ScanArgs sa{};
   sa.sizes = ea.sizes;
@@ -759,8 +756,8 @@ int compress_impl(const void* in, int ndims, const uint64_t* dims, int dtype, do
   for (int i = 0; i < 16; ++i) g_stats.pass_items[i] = hc->pass_items[i];
   for (int i = 0; i < 16; ++i) g_stats.phase_cycles[i] = hc->phase[i];
   for (int i = 0; i < 16; ++i) g_stats.pass_us[i] = (float)(hc->pass_ns[i] * 1e-3);
-  if (g_timing >= 2)  // diagnostic: dense-pass cycles per phase (levels, s write, border) in phase_cycles[5..7]
-    for (int i = 1; i < 4; ++i) g_stats.phase_cycles[4 + i] += hc->dense_cycles[i];
+  if (g_timing >= 2)  // diagnostic: k_tiles visit counters (tile engine) / k_sweep dense-pass cycles in phase_cycles[8..11]
+    for (int i = 0; i < 4; ++i) g_stats.phase_cycles[8 + i] = hc->dense_cycles[i];
   uint32_t err = hc->err;
   if (err & kErrPlanes) return kRetryU32;  // a subbin above 8 planes: the caller re-runs on the u32 engine
   if (hc->passes >= (unsigned long long)(1 << 20) &&
@@ -840,7 +837,7 @@ int lopc_repair_ex(const void* in, int ndims, const uint64_t* dims, int dtype, d
   Timer tm;
   for (int engine = g_engine;;) {
     CK(cudaMemsetAsync(ws, 0, L.zero_end, st));
-    if ((rc = run_repair(sh, in, eps, ws, L, st, tm, engine))) return rc;
+    if ((rc = run_repair(sh, in, eps, ws, L, st, tm, engine, true))) return rc;
     CK(cudaMemcpyAsync(hc, ws + L.ctr, sizeof(Counters), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     if (!(hc->err & kErrPlanes)) break;

@@ -725,7 +725,67 @@ struct EncodeArgs {
   uint64_t d0, d1, d2;
   double xlim;   // |x| < xlim proves x regular (finite, |b| <= BINMAX): the subbin CTAs' escape test
   float xlim32;  // the same bound as a float (f32 data)
+  // Subbin planes (tile engine, lopc_tiles.cuh): 8 u32 per 32-point x-segment
+  // (word b = bit b of the segment's 32 subbins); null: u32 subbins in s.
+  // With planes, the escape bits come from word esc_word of each flag
+  // segment (k_quant_flags) and the bound self-check a4 runs in the bin
+  // CTAs, which hold x and the bins already: the subbin CTAs read no x.
+  const uint32_t* sp;
+  const uint32_t* flags;
+  int64_t nseg;
+  int sw, esc_word;
 };
+
+// Subbin planes b0 .. b0+NPL-1 (and, with ESC, the escape bits) of the 32
+// linear elements starting at row `row`, column x (bits past n are 0): one
+// x-segment when rows are whole segments (d2 a multiple of 32), else up to
+// three segment pieces across a row end.  `left` = n - (linear index of the
+// first element).
+template <int NPL>
+__device__ __forceinline__ void gather_group(const EncodeArgs& a, uint64_t row, uint32_t x, uint64_t left, int b0,
+                                             bool want_esc, uint32_t (&pl)[NPL], uint32_t& esc) {
+#pragma unroll
+  for (int b = 0; b < NPL; ++b) pl[b] = 0;
+  esc = 0;
+  const uint32_t d2 = (uint32_t)a.d2;
+  for (uint32_t o = 0; o < 32 && left > 0;) {
+    const uint32_t seg = x >> 5, bit = x & 31;
+    uint32_t take = 32 - bit < 32 - o ? 32 - bit : 32 - o;
+    if (d2 - x < take) take = d2 - x;
+    if (left < take) take = (uint32_t)left;
+    const uint32_t m = take >= 32 ? 0xffffffffu : ((1u << take) - 1u);
+    const size_t rs = (size_t)row * (size_t)a.nseg + seg;
+    uint32_t w[NPL];
+    if constexpr (NPL == 4) {
+      const uint4 v = __ldg(reinterpret_cast<const uint4*>(a.sp + rs * 8 + b0));
+      w[0] = v.x, w[1] = v.y, w[2] = v.z, w[3] = v.w;
+    } else {
+      static_assert(NPL == 2, "2 or 4 planes per thread");
+      const uint2 v = __ldg(reinterpret_cast<const uint2*>(a.sp + rs * 8 + b0));
+      w[0] = v.x, w[1] = v.y;
+    }
+#pragma unroll
+    for (int b = 0; b < NPL; ++b) pl[b] |= ((w[b] >> bit) & m) << o;
+    if (want_esc) esc |= ((__ldg(a.flags + rs * (size_t)a.sw + a.esc_word) >> bit) & m) << o;
+    o += take;
+    left -= take;
+    x += take;
+    if (x == d2) {
+      x = 0;
+      ++row;
+    }
+  }
+}
+
+// One element's subbin from the planes (the raw-fallback rebuild; rare).
+__device__ __forceinline__ uint32_t subbin_at(const EncodeArgs& a, uint64_t i) {
+  const uint64_t row = i / a.d2, x = i - row * a.d2;
+  const uint32_t* p = a.sp + ((size_t)row * (size_t)a.nseg + (x >> 5)) * 8;
+  uint32_t v = 0;
+#pragma unroll
+  for (int b = 0; b < 8; ++b) v |= ((__ldg(p + b) >> (x & 31)) & 1u) << b;
+  return v;
+}
 
 // xlim = 2^30 eps (f32 data) / 2^49 eps (f64): |x| below it gives |x/eps| < 2^30
 // (2^49), so |b| <= 2^30 < BINMAX = 2^31 - 2 (|b| <= 2^49 < 2^50), and x is
@@ -816,17 +876,54 @@ __global__ void __launch_bounds__(kCodecThreads, ROLE == 2 ? LOPC_SUBS_CTAS : LO
   const uint32_t cnt = (uint32_t)min((uint64_t)W, a.n - e0);
   const T* X = static_cast<const T*>(a.x) + e0;
   const uint32_t* S = a.s + e0;
+  constexpr int G = W / 32;  // 32-element groups of the chunk
+  uint32_t* PL = reinterpret_cast<uint32_t*>(sm.O);  // planes mode: [b * G + g] subbin planes, [8G + g] escapes
+  if (tid == 0) {
+    sm.misc[1] = 0;  // OR over the chunk of the plane-nonzero masks
+    sm.misc[2] = 0;  // any escape in the chunk
+  }
   __syncthreads();
+  if (a.sp) {  // gather the chunk's subbin planes and escape bits (both roles)
+    // all threads: group g = tid mod G, planes [b0, b0 + NPL) (f32: 2 x 4
+    // planes, f64: 4 x 2 planes per group); the first thread of a group
+    // also takes its escape bits.  The group's (row, x): one 64-bit division
+    // per CTA, then 32-bit steps (rows of d2 < 2^32 points).
+    constexpr int NPL = 8 * G / kCodecThreads;
+    const int g = tid % G, b0 = (tid / G) * NPL;
+    const uint64_t r0 = e0 / a.d2;
+    const uint32_t xg = (uint32_t)(e0 - r0 * a.d2) + 32u * (uint32_t)g, d2 = (uint32_t)a.d2;
+    const uint32_t dr = xg / d2;
+    const uint64_t i0 = e0 + 32ull * g;
+    uint32_t pl[NPL], esc;
+    gather_group<NPL>(a, r0 + dr, xg - dr * d2, i0 < a.n ? a.n - i0 : 0, b0, b0 == 0, pl, esc);
+    uint32_t nzp = 0;
+#pragma unroll
+    for (int b = 0; b < NPL; ++b) {
+      PL[(b0 + b) * G + g] = pl[b];
+      nzp |= (uint32_t)(pl[b] != 0u) << (b0 + b);
+    }
+    if (b0 == 0) PL[8 * G + g] = esc;
+    nzp = __reduce_or_sync(0xffffffffu, nzp);
+    const uint32_t ae = __reduce_or_sync(0xffffffffu, esc);
+    if (lane == 0) {
+      if (nzp) atomicOr(&sm.misc[1], nzp);
+      if (ae) atomicOr(&sm.misc[2], 1u);
+    }
+    __syncthreads();
+    pc.mark(a.ctr, 0);
+  }
 
   // --- a1: re-quantize; bin words (ROLE 1) or subbin words + a4 queue (ROLE 2).
   // Thread slot k = 4v + q holds element 4 (v * NT + tid) + q.  Elements past
   // the chunk's end load as x = 0, s = 0, whose words are 0 (b(0) = 0), the
   // zero padding of G23.
   constexpr int NV = PER / 2;  // two halves of PER slots (register budget)
-  uint32_t qmask = 0, nesc = 0;
+  uint32_t qmask = 0, nesc = 0, bad4 = 0;
+  const uint32_t pmk = sm.misc[1];
+  const int npl = pmk ? 32 - __clz(pmk) : 0;  // planes mode: non-zero subbin planes of the chunk
   U orw = 0;
 #pragma unroll 1
-  for (int hh = 0; hh < 2; ++hh) {
+  for (int hh = 0; hh < ((SUBS && a.sp) ? 0 : 2); ++hh) {
     T xs[NV];
     uint32_t ss[NV];
     if (a.vec && cnt == (uint32_t)W) {
@@ -872,6 +969,30 @@ __global__ void __launch_bounds__(kCodecThreads, ROLE == 2 ? LOPC_SUBS_CTAS : LO
               const int64_t r = quantize_slow<T>(xs[4 * v + q], a.eps, a.inv);
               nesc += r == kEscape;
               wv[q] = r == kEscape ? VT<T>::kSentinel : (U)(I)r;
+            }
+          }
+        }
+        if (a.sp && npl) {
+          // a4 (planes mode), here where x and the bins are in registers:
+          // key(lo(b)) + s <= key(x) for the elements with s > 0 (proof (i),
+          // S:151-159).  The 4 subbins as bytes of s4: plane b's nibble of
+          // the 4 elements spread to bit b of each byte (bit q -> bit 8q by
+          // one multiply: q + 7q, no carries).
+          const int e4 = 4 * ((hh * (NV / 4) + v) * kCodecThreads + tid);
+          const uint32_t g = (uint32_t)e4 >> 5, sh = (uint32_t)e4 & 31u;
+          uint32_t s4 = 0;
+          for (int b = 0; b < npl; ++b) s4 |= ((((PL[b * G + g] >> sh) & 0xfu) * 0x00204081u) & 0x01010101u) << b;
+          if (s4) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const uint32_t sq = (s4 >> (8 * q)) & 0xffu;
+              if (sq) {
+                if (wv[q] == VT<T>::kSentinel)
+                  bad4 = 1;  // an escaped point has no arcs, so no subbin
+                else if ((int64_t)lo_key<T>((int64_t)(I)wv[q], a.eps) + (int64_t)sq >
+                         (int64_t)key_of((U)as_bits(xs[4 * v + q])))
+                  bad4 = 1;
+              }
             }
           }
         }
@@ -926,9 +1047,27 @@ __global__ void __launch_bounds__(kCodecThreads, ROLE == 2 ? LOPC_SUBS_CTAS : LO
   } else {
     const uint32_t esc = __reduce_add_sync(0xffffffffu, nesc);
     if (lane == 0 && esc) atomicAdd(&a.ctr->escapes, (unsigned long long)esc);
+    if (__any_sync(0xffffffffu, bad4) && lane == 0) atomicOr(&a.ctr->err, kErrBound);
+  }
+  if (SUBS && a.sp && sm.misc[2]) {
+    // planes mode, a chunk with escapes: words = subbins from the planes,
+    // raw bits of x at the escapes (the only x this CTA reads)
+    for (int i = tid; i < W; i += kCodecThreads) {
+      const int g = i >> 5, bit = i & 31;
+      uint32_t sv = 0;
+#pragma unroll
+      for (int b = 0; b < 8; ++b) sv |= ((PL[b * G + g] >> bit) & 1u) << b;
+      const U w = ((PL[8 * G + g] >> bit) & 1u) ? (U)as_bits(X[i]) : (U)sv;
+      WD[swz<U>(i)] = w;
+      orw |= w;
+    }
+    const uint32_t olo = __reduce_or_sync(0xffffffffu, (uint32_t)orw);
+    const uint32_t ohi = sizeof(U) == 8 ? __reduce_or_sync(0xffffffffu, (uint32_t)((uint64_t)orw >> 32)) : 0u;
+    if (lane == 0 && (olo | ohi)) atomicOr(&sm.pm[0], ((unsigned long long)ohi << 32) | olo);
   }
   __syncthreads();
   pc.mark(a.ctr, 1);
+
 
   uint32_t size;
   if constexpr (SUBS) {
@@ -946,12 +1085,23 @@ __global__ void __launch_bounds__(kCodecThreads, ROLE == 2 ? LOPC_SUBS_CTAS : LO
     if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(&a.ctr->err, kErrBound);
     pc.mark(a.ctr, 2);
     // --- a6: subbins: BIT_k -> RZE_k -> RZE_1 ----------------------
-    const unsigned long long ow = sm.pm[0];
-    int P = ow ? 64 - __clzll((long long)ow) : 0;
-    if (P <= 8)
-      bit_forward_ballot<U>(sm.Wd, W, P);
-    else
-      P = bit_forward_inplace<U, false>(sm.Wd, W, &sm.pm[1]);
+    int P;
+    if (a.sp && !sm.misc[2]) {
+      // planes mode without escapes: BIT_k of the subbin words IS the
+      // gathered planes (planes >= 8 are zero): copy the P non-zero ones
+      const uint32_t pmk = sm.misc[1];
+      P = pmk ? 32 - __clz(pmk) : 0;
+      uint32_t* planes = reinterpret_cast<uint32_t*>(sm.Wd);
+      for (int t = tid; t < P * G; t += kCodecThreads) planes[t] = PL[t];
+      __syncthreads();
+    } else {
+      const unsigned long long ow = sm.pm[0];
+      P = ow ? 64 - __clzll((long long)ow) : 0;
+      if (P <= 8)
+        bit_forward_ballot<U>(sm.Wd, W, P);
+      else
+        P = bit_forward_inplace<U, false>(sm.Wd, W, &sm.pm[1]);
+    }
     pc.mark(a.ctr, 3);
     const uint32_t l1 = rze_enc(sm.Wd, kChunkBytes, K, sm.O, 0xffffffffu, sm.R, (uint32_t)P * PB);
     for (uint32_t t = l1 + tid; t < ((l1 + 15) & ~15u) + 16; t += kCodecThreads) sm.O[t] = 0;
@@ -992,7 +1142,7 @@ __global__ void __launch_bounds__(kCodecThreads, ROLE == 2 ? LOPC_SUBS_CTAS : LO
       if ((uint32_t)i < cnt) {
         I b;
         if (quantize_fast<T>(X[i], a.inv32, a.eps, a.inv, b))
-          w = SUBS ? (U)S[i] : (U)b;
+          w = SUBS ? (U)(a.sp ? subbin_at(a, e0 + (uint64_t)i) : S[i]) : (U)b;
         else
           w = SUBS ? (U)as_bits(X[i]) : VT<T>::kSentinel;
       }

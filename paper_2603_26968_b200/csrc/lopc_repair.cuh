@@ -53,7 +53,7 @@ struct Geo<3> {
   static constexpr int HZ = TZ + 2, HY = TY + 2, HX = TX + 2;
   static constexpr int ZH = 1;
   static constexpr int D = 7;   // +e offsets (G2)
-  static constexpr int SW = 16; // words per 32-point flag segment (14 used)
+  static constexpr int SW = 16; // words per 32-point flag segment (14 slots, word 14 = escapes)
 };
 template <>
 struct Geo<2> {
@@ -61,7 +61,7 @@ struct Geo<2> {
   static constexpr int HZ = 1, HY = TY + 2, HX = TX + 2;
   static constexpr int ZH = 0;
   static constexpr int D = 3;
-  static constexpr int SW = 8;  // 6 used
+  static constexpr int SW = 8;  // 6 slots, word 6 = escapes
 };
 
 #ifndef LOPC_SWEEP_CTAS
@@ -549,6 +549,9 @@ __global__ void __launch_bounds__(kRepairThreads, sizeof(T) == 4 ? LOPC_QF_CTAS 
       wv[j] = __ballot_sync(0xffffffffu, arc);
     }
     const Idx gz = z0 + lz, gy = y0 + ly;
+    // word SW-2: escape bits (non-regular in-grid points: NaN, +-Inf, |b| >
+    // BINMAX), read by the subbin encoder in planes mode instead of x
+    wv[G::SW - 2] = __ballot_sync(0xffffffffu, lok == kHigh && gz < d0 && gy < d1 && x0 + lane < d2);
     if (lane == 0 && gz < d0 && gy < d1) {
       const Idx rb = (gz * d1 + gy) * d2 + x0;
       if (rb < (Idx)a.own_lo || rb + 32 > (Idx)a.own_hi) {

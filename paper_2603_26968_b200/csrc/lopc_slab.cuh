@@ -273,6 +273,15 @@ int nccl_load() {
 
 int err_rank(int rc) { return rc < 0 ? -rc : 0; }
 
+// Test hook: LOPC_FAULT_RANK=r and LOPC_FAULT_ROUND=k make rank r fail
+// locally after repair round k (0 = after the first sweep), to exercise the
+// slab mode's error agreement.  Off unless both are set.
+bool fault_injected(int rank, int round) {
+  static const int fr = getenv("LOPC_FAULT_RANK") ? atoi(getenv("LOPC_FAULT_RANK")) : -1;
+  static const int fk = getenv("LOPC_FAULT_ROUND") ? atoi(getenv("LOPC_FAULT_ROUND")) : -1;
+  return fr >= 0 && fk >= 0 && rank == fr && round == fk;
+}
+
 }  // namespace
 
 struct lopc_comm {
@@ -449,24 +458,41 @@ int lopc_compress_slab(lopc_comm* comm, const void* in_slab, int ndims, const ui
     if (G.ghi) CK(cudaMemcpyAsync(sl.ghost_hi_ptr(sl.xbox(), g.k), sl.recv_hi(), G.ghi * g.k, cudaMemcpyDeviceToDevice, st));
   }
   tm.mark();  // 1
-  if ((rc = launch_quant_flags(G.box, sl.ra, sl.lay.L, st))) return rc;
+  // From here on every rank takes part in every collective of the schedule
+  // whatever happens locally: a local failure (lrc) skips this rank's work,
+  // is summed into the round's allreduce (all ranks leave the loop together)
+  // and reaches every rank's return code through the final allgather.  Only
+  // a failing NCCL call itself returns at once (the communicator is then
+  // unusable; the caller must tear the job down).
+  int lrc = launch_quant_flags(G.box, sl.ra, sl.lay.L, st);
   tm.mark();  // 2
-  if ((rc = launch_sweep(G.box, sl.ra, sl.lay.L, st))) return rc;
+  if (!lrc) lrc = launch_sweep(G.box, sl.ra, sl.lay.L, st);
+  if (!lrc && fault_injected(rank, 0)) lrc = LOPC_E_INTERNAL;
   uint64_t rounds = 1;
   while (world > 1) {
     if ((rc = halo(reinterpret_cast<uint8_t*>(sl.s()), 4, ncclUint32))) return rc;
-    if ((rc = sl.inject())) return rc;
-    uint64_t* sum = reinterpret_cast<uint64_t*>(sl.ws + sl.lay.ctr_sum);
-    NK(g_nccl.AllReduce(&sl.dctr()->ghost_changed, sum, 1, ncclUint64, ncclSum, comm->comm, st));
-    uint64_t hs = 0;
-    CK(cudaMemcpyAsync(&hs, sum, 8, cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
-    if (hs == 0) break;
-    if ((rc = sl.sweep_sparse())) return rc;
+    if (!lrc) lrc = sl.inject();
+    if (!lrc && fault_injected(rank, (int)rounds)) lrc = LOPC_E_INTERNAL;
+    // round agreement: sum over ranks of (ghosts raised, local failures)
+    uint64_t* sum = reinterpret_cast<uint64_t*>(sl.ws + sl.lay.ctr_sum);  // [0, 1] in, [2, 3] out
+    if (cudaMemcpyAsync(sum, &sl.dctr()->ghost_changed, 8, cudaMemcpyDeviceToDevice, st) != cudaSuccess ||
+        cudaMemsetAsync(sum + 1, 0, 8, st) != cudaSuccess || (lrc && cudaMemsetAsync(sum + 1, 1, 1, st) != cudaSuccess))
+      lrc = lrc ? lrc : LOPC_E_CUDA;
+    NK(g_nccl.AllReduce(sum, sum + 2, 2, ncclUint64, ncclSum, comm->comm, st));
+    uint64_t hs[2] = {0, 1};
+    if (cudaMemcpyAsync(hs, sum + 2, 16, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+        cudaStreamSynchronize(st) != cudaSuccess)
+      return set_cuda_error(cudaGetLastError(), "slab round agreement");
+    if (hs[1] != 0) {  // some rank failed: everyone stops here
+      if (!lrc) lrc = LOPC_E_INTERNAL;  // the failing rank's own code wins in the final allgather
+      break;
+    }
+    if (hs[0] == 0) break;
+    if (!lrc) lrc = sl.sweep_sparse();
     ++rounds;
   }
   tm.mark();  // 3
-  if ((rc = sl.encode(static_cast<uint8_t*>(out_local), *out_local_bytes, &tm))) return rc;  // mark 4
+  if (!lrc) lrc = sl.encode(static_cast<uint8_t*>(out_local), *out_local_bytes, &tm);  // mark 4
   tm.mark();  // 5
   CK(cudaMemcpyAsync(hc, sl.dctr(), sizeof(Counters), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
@@ -478,7 +504,11 @@ int lopc_compress_slab(lopc_comm* comm, const void* in_slab, int ndims, const ui
     g_stats.ms_place = tm.ms(4, 5);
     g_stats.ms_total = tm.ms(0, 5);
   }
-  uint64_t mine[2] = {hc->total_bytes, (uint64_t)err_rank(map_err(hc->err))};
+  uint32_t herr = hc->err;
+  if (hc->passes >= (unsigned long long)sl.ra.max_passes && hc->list_count[(hc->passes + 1) % 3] != 0)
+    herr |= kErrPassCap;  // a repair that did not converge is never encoded silently
+  const int local = lrc ? lrc : map_err(herr & ~kErrNoSpace);
+  uint64_t mine[2] = {hc->total_bytes, (uint64_t)err_rank(local)};
   std::vector<uint64_t> all(2 * world);
   if (world > 1) {
     uint64_t* d = reinterpret_cast<uint64_t*>(sl.ws + sl.lay.ctr_sum);
@@ -504,8 +534,11 @@ int lopc_compress_slab(lopc_comm* comm, const void* in_slab, int ndims, const ui
   g_stats.total_bytes = off;
   g_stats.inner_iters = rounds;  // slab mode: repair rounds (halo exchanges + 1)
   g_stats.launches = (uint32_t)(2 + 3 * (rounds - 1) + 2 + 3);
-  if (worst) return -(int)worst;
   const uint64_t need = 8 * G.C_local + mine[0];
+  if (worst) {
+    if (-(int)worst == LOPC_E_NOSPACE) *out_local_bytes = need;  // lopc.h: NOSPACE reports the size needed
+    return -(int)worst;
+  }
   if (need > *out_local_bytes) {
     *out_local_bytes = need;
     return LOPC_E_NOSPACE;

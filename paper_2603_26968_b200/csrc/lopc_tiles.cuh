@@ -10,15 +10,17 @@
 // (reading G14).  The schedule is B200-shaped, not the paper's point worklist
 // (P:218-220):
 //
-//   pass 1        every tile of tiling 0 (8x8x32 in 3D, 64x32 in 2D: one
-//                 warp each), halo and seeds 0 (the r1 dense pass).
+//   pass 1        every tile of tiling 0 (4x8x32 in 3D, 32x32 in 2D: one
+//                 warp each, lane = row), halo and seeds 0.
 //   pass q >= 2   the ACTIVE tiles of tiling (q-1) mod 2.  Tiling 1 is
 //                 tiling 0 shifted by half a tile in z and y (x stays
 //                 32-aligned so a tile row is one flag / plane segment): a
 //                 chain that crosses a tile border in one tiling runs inside
 //                 a tile of the other (overlapping-domain / alternating
 //                 Schwarz relaxation).  A tile of pass q+1 is active iff one
-//                 of its points has a star neighbour that changed in pass q;
+//                 of its points is an out-of-tile star neighbour of a point
+//                 that changed in pass q (successors inside the changed
+//                 point's own tile are satisfied by that tile's fixpoint);
 //                 pass q builds that list (per-tile mark words + an
 //                 append-only list) and processes its own list in reverse
 //                 build order, so consecutive passes sweep in opposite
@@ -57,39 +59,43 @@ constexpr int kTileWarps = kTileThreads / 32;
 #define LOPC_TILE_CTAS 3
 #endif
 
+// Tile geometry of the repair: 32 rows of 32 points, one row per lane
+// (3D 4 x 8 x 32, 2D 32 x 32); the box adds the one-cell halo in z and y.
 template <int NDIM>
-struct TBox {
-  using G = Geo<NDIM>;
-  static constexpr int BY = G::TY + 2;                 // box rows along y (halo included)
-  static constexpr int NB = (G::TZ + 2 * G::ZH) * BY;  // box rows
-  static constexpr int NH = NDIM == 3 ? 34 : 2;        // halo rows the star reaches
-  static constexpr int SZ = NDIM == 3 ? G::TZ / 2 : 0; // tiling 1 shift (z, y)
-  static constexpr int SY = G::TY / 2;
-  __host__ __device__ static constexpr int idx(int bz, int by) { return (bz + G::ZH) * BY + (by + 1); }
-  // halo row h -> box coordinates (bz, by): the rows a star offset of a tile
-  // row reaches: z0-1 plane (y0-1 .. y0+TY-1), z0+TZ plane (y0 .. y0+TY),
-  // y0-1 and y0+TY rows of every tile plane
+struct TG {
+  static constexpr int TZ = NDIM == 3 ? 4 : 1, TY = NDIM == 3 ? 8 : 32, ZH = NDIM == 3 ? 1 : 0;
+  static constexpr int D = NDIM == 3 ? 7 : 3;          // +e offsets (G2)
+  static constexpr int SW = NDIM == 3 ? 16 : 8;        // flag words per segment (Geo<NDIM>::SW)
+  static constexpr int BY = TY + 2;                    // box rows along y
+  static constexpr int NB = (TZ + 2 * ZH) * BY;        // box rows
+  static constexpr int NH = NDIM == 3 ? 2 * (TY + 1) + 2 * TZ : 2;  // halo rows a star offset reaches (26 / 2)
+  static constexpr int SZ = TZ / 2, SY = TY / 2;       // tiling 1 shift (z, y)
+  __host__ __device__ static constexpr int idx(int bz, int by) { return (bz + ZH) * BY + (by + 1); }
+  // halo row h -> box coordinates: the z0-1 plane (y0-1 .. y0+TY-1), the
+  // z0+TZ plane (y0 .. y0+TY), then the y0-1 and y0+TY rows of every plane
   __host__ __device__ static void halo(int h, int& bz, int& by) {
     if (NDIM == 2) {
       bz = 0;
-      by = h == 0 ? -1 : G::TY;
+      by = h == 0 ? -1 : TY;
       return;
     }
-    if (h < 9) {
+    if (h <= TY) {
       bz = -1;
       by = h - 1;
-    } else if (h < 18) {
-      bz = G::TZ;
-      by = h - 9;
-    } else if (h < 26) {
-      bz = h - 18;
+    } else if (h <= 2 * TY + 1) {
+      bz = TZ;
+      by = h - (TY + 1);
+    } else if (h < 2 * TY + 2 + TZ) {
+      bz = h - (2 * TY + 2);
       by = -1;
     } else {
-      bz = h - 26;
-      by = G::TY;
+      bz = h - (2 * TY + 2 + TZ);
+      by = TY;
     }
   }
 };
+static_assert(TG<3>::TZ * TG<3>::TY == 32 && TG<2>::TY == 32, "one tile row per lane");
+static_assert(TG<3>::NH <= 32, "one halo row per lane");
 
 struct TileArgs {
   const uint32_t* flags;  // bit-plane flags (k_quant_flags), SW words per segment
@@ -105,129 +111,74 @@ struct TileArgs {
 };
 
 struct TileWarpSmem {
-  uint32_t lv[2][TBox<3>::NB];  // level words of the box rows, [L & 1]
-  uint8_t ed[2][TBox<3>::NB];   // edge level bits: bit 0 = x0-1, bit 1 = x0+32
-  uint32_t hp[TBox<3>::NH][kSP];
-  uint8_t he[TBox<3>::NH][2];   // halo rows' edge subbins (x0-1, x0+32)
+  uint32_t lv[2][TG<3>::NB];  // level words of the box rows, [L & 1]
+  uint8_t ed[2][TG<3>::NB];   // edge level bits: bit 0 = x0-1, bit 1 = x0+32
+  uint32_t hp[kSP][32];       // halo row planes, [plane][lane] (register relief)
+  uint8_t hidx[32];           // box row of lane's halo row (kept here: re-deriving it per level costs ~20 instructions)
 };
 
-// s >= L on bit-sliced planes (L uniform across the warp)
-__device__ __forceinline__ uint32_t planes_ge(const uint32_t (&p)[kSP], uint32_t L) {
-  uint32_t ge = 0, eq = 0xffffffffu;
+// s >= L on bit-sliced planes, branch-free: no borrow out of s - L
+template <int NP>
+__device__ __forceinline__ uint32_t planes_ge(const uint32_t (&p)[NP], uint32_t L) {
+  uint32_t borrow = 0;
 #pragma unroll
-  for (int b = kSP - 1; b >= 0; --b) {
-    if ((L >> b) & 1u)
-      eq &= p[b];
-    else
-      ge |= eq & p[b];
+  for (int b = 0; b < NP; ++b) {
+    const uint32_t l = 0u - ((L >> b) & 1u);  // bit b of L as a mask
+    // borrow' = (~p & l) | (~(p ^ l) & borrow)
+    borrow = (~p[b] & l) | (~(p[b] ^ l) & borrow);
   }
-  return ge | eq;
+  // values < 2^NP: L >= 2^NP is above all of them
+  return (L >> NP) ? 0u : ~borrow;
 }
 
 // One row's subbin planes (x-aligned segment tx) and the subbins of its x
 // halo points x0-1, x0+32 (bits 31 / 0 of the neighbouring segments).
 // L2 loads: other tiles write planes during the pass.
-__device__ __forceinline__ void load_sp_row(const TileArgs& a, int64_t gz, int64_t gy, int64_t tx, uint32_t (&p)[kSP],
-                                            uint32_t& eL, uint32_t& eR) {
+__device__ __forceinline__ void load_sp_row(const TileArgs& a, bool in, int64_t gz, int64_t gy, int64_t tx,
+                                            uint32_t (&p)[kSP], uint32_t& eL, uint32_t& eR) {
 #pragma unroll
   for (int b = 0; b < kSP; ++b) p[b] = 0;
   eL = eR = 0;
-  if (gz < 0 || gz >= a.d0 || gy < 0 || gy >= a.d1) return;
+  if (!in || gz < 0 || gz >= a.d0 || gy < 0 || gy >= a.d1) return;
   const uint4* r4 = reinterpret_cast<const uint4*>(a.sp + ((size_t)(gz * a.d1 + gy) * (size_t)a.nseg + (size_t)tx) * kSP);
+  const bool hl = tx > 0, hr = tx + 1 < a.nseg;
   const uint4 c0 = __ldcg(r4), c1 = __ldcg(r4 + 1);
+  const uint4 l0 = hl ? __ldcg(r4 - 2) : make_uint4(0, 0, 0, 0), l1 = hl ? __ldcg(r4 - 1) : make_uint4(0, 0, 0, 0);
+  const uint4 q0 = hr ? __ldcg(r4 + 2) : make_uint4(0, 0, 0, 0), q1 = hr ? __ldcg(r4 + 3) : make_uint4(0, 0, 0, 0);
   p[0] = c0.x, p[1] = c0.y, p[2] = c0.z, p[3] = c0.w, p[4] = c1.x, p[5] = c1.y, p[6] = c1.z, p[7] = c1.w;
-  if (tx > 0) {
-    const uint4 l0 = __ldcg(r4 - 2), l1 = __ldcg(r4 - 1);
-    eL = (l0.x >> 31) | ((l0.y >> 31) << 1) | ((l0.z >> 31) << 2) | ((l0.w >> 31) << 3) | ((l1.x >> 31) << 4) |
-         ((l1.y >> 31) << 5) | ((l1.z >> 31) << 6) | ((l1.w >> 31) << 7);
-  }
-  if (tx + 1 < a.nseg) {
-    const uint4 q0 = __ldcg(r4 + 2), q1 = __ldcg(r4 + 3);
-    eR = (q0.x & 1u) | ((q0.y & 1u) << 1) | ((q0.z & 1u) << 2) | ((q0.w & 1u) << 3) | ((q1.x & 1u) << 4) |
-         ((q1.y & 1u) << 5) | ((q1.z & 1u) << 6) | ((q1.w & 1u) << 7);
-  }
+  eL = (l0.x >> 31) | ((l0.y >> 31) << 1) | ((l0.z >> 31) << 2) | ((l0.w >> 31) << 3) | ((l1.x >> 31) << 4) |
+       ((l1.y >> 31) << 5) | ((l1.z >> 31) << 6) | ((l1.w >> 31) << 7);
+  eR = (q0.x & 1u) | ((q0.y & 1u) << 1) | ((q0.z & 1u) << 2) | ((q0.w & 1u) << 3) | ((q1.x & 1u) << 4) |
+       ((q1.y & 1u) << 5) | ((q1.z & 1u) << 6) | ((q1.w & 1u) << 7);
 }
 
-// Exact fixpoint of one tile (one warp).  SEEDED: current subbins are lower
-// bounds and the halo holds the neighbours' current subbins; otherwise both
-// are 0 (pass 1).  Writes changed rows, marks the tiles of the other tiling
-// that hold a star neighbour of a changed point, returns the number of
-// changed points (lane-summed by the caller).
-template <int NDIM, bool SEEDED>
-__device__ __forceinline__ uint32_t tile_fix(const TileArgs& a, int tiling, uint32_t tz, uint32_t ty, uint32_t tx,
-                                             TileWarpSmem& W, int next_pass, uint32_t& my_max) {
-  using G = Geo<NDIM>;
-  using B = TBox<NDIM>;
+// The level loop of one tile on NP bit planes: cnt = the new subbins (planes
+// >= NP zero).  Returns L = 1 + the highest non-empty level, or -1 when a
+// level reaches 2^NP - 1 (the count would not fit NP planes).
+template <int NDIM, bool SEEDED, int NP>
+__device__ __forceinline__ int tile_levels(const uint32_t (&F)[2 * TG<NDIM>::D], const uint32_t (&sp)[kSP], uint32_t eL,
+                                           uint32_t eR, uint32_t hL, uint32_t hR, int bi, int hbi, int lz, int ly,
+                                           TileWarpSmem& W, uint32_t (&cnt)[kSP], bool prof, int& first_new) {
+  using G = TG<NDIM>;
   constexpr int D = G::D;
-  constexpr int SW = G::SW;
   constexpr int JX = D;  // the -x slot (0,0,-1): weight 0, closed by xfill
   const int lane = threadIdx.x & 31;
-  const int64_t d0 = a.d0, d1 = a.d1, d2 = a.d2;
-  const size_t nseg = (size_t)a.nseg;
-  const int64_t z0 = (int64_t)tz * G::TZ - (tiling ? B::SZ : 0);
-  const int64_t y0 = (int64_t)ty * G::TY - (tiling ? B::SY : 0);
-  const int64_t x0 = (int64_t)tx * G::TX;
-  const uint32_t vmask = x0 + 32 <= d2 ? 0xffffffffu : ((1u << (uint32_t)(d2 - x0)) - 1u);
-
-  // own rows rr = lane + 32 i: flags, seeds, edge subbins
-  uint32_t F[2][2 * D];
-  uint32_t sp[2][kSP];
-  uint32_t eL[2], eR[2];
-  int lz[2], ly[2], bi[2];
-  bool rin[2];
-#pragma unroll
-  for (int i = 0; i < 2; ++i) {
-    const int rr = lane + 32 * i;
-    lz[i] = rr / G::TY;
-    ly[i] = rr % G::TY;
-    bi[i] = B::idx(lz[i], ly[i]);
-    const int64_t gz = z0 + lz[i], gy = y0 + ly[i];
-    rin[i] = gz >= 0 && gz < d0 && gy >= 0 && gy < d1;
-    const uint4* seg = reinterpret_cast<const uint4*>(a.flags + ((size_t)(rin[i] ? gz * d1 + gy : 0) * nseg + tx) * SW);
-#pragma unroll
-    for (int q = 0; q < SW / 4; ++q) {
-      const uint4 w = rin[i] ? __ldg(seg + q) : make_uint4(0, 0, 0, 0);
-      const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
-#pragma unroll
-      for (int t = 0; t < 4; ++t)
-        if (4 * q + t < 2 * D) F[i][4 * q + t] = ws[t];
-    }
-    if (SEEDED) {
-      load_sp_row(a, gz, gy, (int64_t)tx, sp[i], eL[i], eR[i]);
-    } else {
-#pragma unroll
-      for (int b = 0; b < kSP; ++b) sp[i][b] = 0;
-      eL[i] = eR[i] = 0;
-    }
-  }
-  // halo rows: planes and edge subbins to shared memory
-  if (SEEDED) {
-    for (int h = lane; h < B::NH; h += 32) {
-      int bz, by;
-      B::halo(h, bz, by);
-      uint32_t p[kSP], l, r;
-      load_sp_row(a, z0 + bz, y0 + by, (int64_t)tx, p, l, r);
-#pragma unroll
-      for (int b = 0; b < kSP; ++b) W.hp[h][b] = p[b];
-      W.he[h][0] = (uint8_t)l;
-      W.he[h][1] = (uint8_t)r;
-    }
-  }
-  // level words of the box: halo rows hold 0 (pass 1) or their level sets
-  for (int t = lane; t < B::NB; t += 32) {
+  (void)lz;
+  (void)ly;
+  // level words of the box: all 0 (pass 1's halo stays 0)
+  for (int t = lane; t < G::NB; t += 32) {
     W.lv[0][t] = 0;
     W.lv[1][t] = 0;
     W.ed[0][t] = 0;
     W.ed[1][t] = 0;
   }
   __syncwarp();
-
-  uint32_t cnt[2][kSP];
+  uint32_t spn[NP];
 #pragma unroll
-  for (int i = 0; i < 2; ++i)
+  for (int b = 0; b < NP; ++b) spn[b] = sp[b];
 #pragma unroll
-    for (int b = 0; b < kSP; ++b) cnt[i][b] = 0;
-  uint32_t X[2] = {0, 0};
+  for (int b = 0; b < kSP; ++b) cnt[b] = 0;
+  uint32_t X = 0;
   int L = 1;
   for (;; ++L) {
     uint32_t* cur = W.lv[L & 1];
@@ -235,130 +186,197 @@ __device__ __forceinline__ uint32_t tile_fix(const TileArgs& a, int tiling, uint
     uint8_t* cE = W.ed[L & 1];
     const uint8_t* pE = W.ed[(L - 1) & 1];
     if (SEEDED) {  // the halo's level sets at L (prv holds L - 1 from the last level)
-      for (int h = lane; h < B::NH; h += 32) {
-        int bz, by;
-        B::halo(h, bz, by);
-        uint32_t p[kSP];
+      if (lane < G::NH) {
+        uint32_t hp[NP];
 #pragma unroll
-        for (int b = 0; b < kSP; ++b) p[b] = W.hp[h][b];
-        const int t = B::idx(bz, by);
-        cur[t] = planes_ge(p, (uint32_t)L);
-        cE[t] = (uint8_t)(((uint32_t)W.he[h][0] >= (uint32_t)L) | (((uint32_t)W.he[h][1] >= (uint32_t)L) << 1));
+        for (int b = 0; b < NP; ++b) hp[b] = W.hp[b][lane];
+        const int hb = W.hidx[lane];
+        cur[hb] = planes_ge<NP>(hp, (uint32_t)L);
+        cE[hb] = (uint8_t)((hL >= (uint32_t)L) | ((hR >= (uint32_t)L) << 1));
       }
-#pragma unroll
-      for (int i = 0; i < 2; ++i) cE[bi[i]] = (uint8_t)((eL[i] >= (uint32_t)L) | ((eR[i] >= (uint32_t)L) << 1));
+      cE[bi] = (uint8_t)((eL >= (uint32_t)L) | ((eR >= (uint32_t)L) << 1));
       __syncwarp();
     }
-    uint32_t P[2];
+    uint32_t pv = SEEDED ? planes_ge<NP>(spn, (uint32_t)L) : 0u;
 #pragma unroll
-    for (int i = 0; i < 2; ++i) {
-      uint32_t pv = SEEDED ? planes_ge(sp[i], (uint32_t)L) : 0u;
-#pragma unroll
-      for (int j = 0; j < D; ++j) {
-        if (L == 1) {
-          pv |= F[i][j];  // from any predecessor (s >= 0) through a w = 1 arc
-        } else {
-          const int t = B::idx(lz[i] + slot_dz<NDIM>(j), ly[i] + slot_dy<NDIM>(j));
-          uint32_t v = prv[t];
-          if (slot_dx<NDIM>(j) > 0) v = (v >> 1) | (SEEDED ? ((uint32_t)(pE[t] >> 1) << 31) : 0u);
-          pv |= F[i][j] & v;
-        }
+    for (int j = 0; j < D; ++j) {
+      if (L == 1) {
+        pv |= F[j];  // from any predecessor (s >= 0) through a w = 1 arc
+      } else {
+        const int t = bi + slot_dz<NDIM>(j) * G::BY + slot_dy<NDIM>(j);
+        uint32_t v = prv[t];
+        if (slot_dx<NDIM>(j) > 0) v = (v >> 1) | (SEEDED ? ((uint32_t)(pE[t] >> 1) << 31) : 0u);
+        pv |= F[j] & v;
       }
-      if (SEEDED) pv |= F[i][JX] & (uint32_t)(cE[bi[i]] & 1u);  // -x neighbour x0-1 (halo) at level L
-      P[i] = pv;
-      X[i] = xfill(pv, F[i][JX]);
     }
+    if (SEEDED) pv |= F[JX] & (uint32_t)(cE[bi] & 1u);  // -x neighbour x0-1 (halo) at level L
+    const uint32_t P = pv;
+    X = xfill(pv, F[JX]);
     // -e closure across rows (weight 0), Jacobi until stable
     for (;;) {
-      cur[bi[0]] = X[0];
-      cur[bi[1]] = X[1];
+      cur[bi] = X;
       __syncwarp();
-      uint32_t Y[2];
+      uint32_t y = P;
 #pragma unroll
-      for (int i = 0; i < 2; ++i) {
-        uint32_t y = P[i];
-#pragma unroll
-        for (int j = D + 1; j < 2 * D; ++j) {
-          const int t = B::idx(lz[i] + slot_dz<NDIM>(j), ly[i] + slot_dy<NDIM>(j));
-          uint32_t v = cur[t];
-          if (slot_dx<NDIM>(j) < 0) v = (v << 1) | (SEEDED ? (uint32_t)(cE[t] & 1u) : 0u);
-          y |= F[i][j] & v;
-        }
-        Y[i] = xfill(y, F[i][JX]);
+      for (int j = D + 1; j < 2 * D; ++j) {
+        const int t = bi + slot_dz<NDIM>(j) * G::BY + slot_dy<NDIM>(j);
+        uint32_t v = cur[t];
+        if (slot_dx<NDIM>(j) < 0) v = (v << 1) | (SEEDED ? (uint32_t)(cE[t] & 1u) : 0u);
+        y |= F[j] & v;
       }
-      const bool ch = (Y[0] != X[0]) || (Y[1] != X[1]);
-      X[0] = Y[0];
-      X[1] = Y[1];
+      const uint32_t Y = xfill(y, F[JX]);
+      const bool ch = Y != X;
+      X = Y;
       __syncwarp();
       if (!__any_sync(0xffffffffu, ch)) break;
     }
-    if (!__any_sync(0xffffffffu, (X[0] | X[1]) != 0)) break;  // Lev_L empty: done
-    if (L == kMaxPlaneLevel) {  // s would not fit 8 planes: the host re-runs on the u32 engine
-      if (lane == 0) atomicOr(&a.ctr->err, kErrPlanes);
-      break;
+    if (!__any_sync(0xffffffffu, X != 0)) break;  // Lev_L empty: done
+    if (SEEDED && prof && first_new == 0 && __any_sync(0xffffffffu, X != planes_ge<NP>(spn, (uint32_t)L)))
+      first_new = L;  // diagnostic: the lowest level where Lev_L != Seed_L
+    if (L == (1 << NP) - 1) return -1;            // the count would not fit NP planes
+    uint32_t carry = X;  // bit-sliced count += Lev_L
+#pragma unroll
+    for (int b = 0; b < NP; ++b) {
+      const uint32_t t = cnt[b] & carry;
+      cnt[b] ^= carry;
+      carry = t;
     }
+  }
+  return L;
+}
+
+// Exact fixpoint of one tile (one warp, lane = tile row).  SEEDED: current
+// subbins are lower bounds and the halo holds the neighbours' current
+// subbins; otherwise both are 0 (pass 1).  Writes changed rows, marks the
+// tiles of the other tiling that hold a star neighbour of a changed point,
+// returns this lane's number of changed points.
+template <int NDIM, bool SEEDED>
+__device__ __forceinline__ uint32_t tile_fix(const TileArgs& a, int tiling, uint32_t tz, uint32_t ty, uint32_t tx,
+                                             TileWarpSmem& W, int next_pass, uint32_t& my_max) {
+  using G = TG<NDIM>;
+  constexpr int D = G::D;
+  constexpr int SW = G::SW;
+  const int lane = threadIdx.x & 31;
+  const int64_t d0 = a.d0, d1 = a.d1, d2 = a.d2;
+  const size_t nseg = (size_t)a.nseg;
+  const int64_t z0 = (int64_t)tz * G::TZ - (tiling ? G::SZ : 0);
+  const int64_t y0 = (int64_t)ty * G::TY - (tiling ? G::SY : 0);
+  const int64_t x0 = (int64_t)tx * 32;
+  const uint32_t vmask = x0 + 32 <= d2 ? 0xffffffffu : ((1u << (uint32_t)(d2 - x0)) - 1u);
+
+  // own row: flags, seeds, edge subbins
+  const int lz = lane / G::TY, ly = lane % G::TY, bi = G::idx(lz, ly);
+  const int64_t gz = z0 + lz, gy = y0 + ly;
+  const bool rin = gz >= 0 && gz < d0 && gy >= 0 && gy < d1;
+  uint32_t F[2 * D];
+  {
+    const uint4* seg = reinterpret_cast<const uint4*>(a.flags + ((size_t)(rin ? gz * d1 + gy : 0) * nseg + tx) * SW);
 #pragma unroll
-    for (int i = 0; i < 2; ++i) {  // bit-sliced count += Lev_L
-      uint32_t carry = X[i];
+    for (int q = 0; q < SW / 4; ++q) {
+      const uint4 w = rin ? __ldg(seg + q) : make_uint4(0, 0, 0, 0);
+      const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
-      for (int b = 0; b < kSP; ++b) {
-        const uint32_t t = cnt[i][b] & carry;
-        cnt[i][b] ^= carry;
-        carry = t;
-      }
+      for (int t = 0; t < 4; ++t)
+        if (4 * q + t < 2 * D) F[4 * q + t] = ws[t];
+    }
+  }
+  uint32_t sp[kSP], eL = 0, eR = 0;
+  // halo row of this lane (lane < NH): planes (to shared memory) and edge subbins
+  uint32_t hL = 0, hR = 0;
+  int hbi = 0;
+  if (SEEDED) {
+    load_sp_row(a, true, gz, gy, (int64_t)tx, sp, eL, eR);
+    int hz, hy;
+    G::halo(lane < G::NH ? lane : 0, hz, hy);
+    hbi = G::idx(hz, hy);
+    uint32_t hp[kSP];
+    load_sp_row(a, lane < G::NH, z0 + hz, y0 + hy, (int64_t)tx, hp, hL, hR);
+#pragma unroll
+    for (int b = 0; b < kSP; ++b) W.hp[b][lane] = hp[b];
+    W.hidx[lane] = (uint8_t)hbi;
+  } else {
+#pragma unroll
+    for (int b = 0; b < kSP; ++b) sp[b] = 0;
+  }
+  // the level sets on NP planes: NP = 4 when every seed and halo subbin is
+  // below 16 (the usual tile), re-run on 8 planes if a level reaches 16
+  uint32_t cnt[kSP];
+  uint32_t big = 0;
+#pragma unroll
+  for (int b = 4; b < kSP; ++b) big |= sp[b] | (SEEDED && lane < G::NH ? W.hp[b][lane] : 0u);
+  big |= (eL | eR | hL | hR) >> 4;
+  int L = 0, first_new = 0;
+  if (!__any_sync(0xffffffffu, big != 0))
+    L = tile_levels<NDIM, SEEDED, 4>(F, sp, eL, eR, hL, hR, bi, hbi, lz, ly, W, cnt, a.prof != 0, first_new);
+  if (L <= 0) {
+    first_new = 0;
+    L = tile_levels<NDIM, SEEDED, kSP>(F, sp, eL, eR, hL, hR, bi, hbi, lz, ly, W, cnt, a.prof != 0, first_new);
+    if (L < 0) {  // s would not fit 8 planes: the host re-runs on the u32 engine
+      if (lane == 0) atomicOr(&a.ctr->err, kErrPlanes);
+      L = kMaxPlaneLevel;
     }
   }
   const uint32_t top = (uint32_t)(L - 1);
   my_max = top > my_max ? top : my_max;
+  if (SEEDED && a.prof && lane == 0) {  // diagnostic (lopc_set_timing(2)): seeded visits, visits with a change,
+    atomicAdd(&a.ctr->dense_cycles[0], 1ull);  // levels run, levels below the first changed one
+    if (first_new) atomicAdd(&a.ctr->dense_cycles[1], 1ull);
+    atomicAdd(&a.ctr->dense_cycles[2], (unsigned long long)L);
+    atomicAdd(&a.ctr->dense_cycles[3], (unsigned long long)(first_new ? first_new - 1 : L));
+  }
 
   // changed points, write-back, marks for the next pass
-  uint32_t nch = 0, zy_mask = 0, xs = 0;
-  const int nt = tiling ^ 1;
-  const int64_t nz0 = z0 - 1 + (nt ? B::SZ : 0), ny0 = y0 - 1 + (nt ? B::SY : 0);
-  const int64_t tzb = nz0 >= 0 ? nz0 / G::TZ : -1, tyb = ny0 >= 0 ? ny0 / G::TY : -1;  // next-tiling tile of (z0-1, y0-1)
+  uint32_t ch = 0;
 #pragma unroll
-  for (int i = 0; i < 2; ++i) {
-    uint32_t ch = 0;
-#pragma unroll
-    for (int b = 0; b < kSP; ++b) ch |= cnt[i][b] ^ sp[i][b];
-    ch &= rin[i] ? vmask : 0u;
-    const int64_t gz = z0 + lz[i], gy = y0 + ly[i];
-    if (SEEDED ? ch != 0u : rin[i]) {  // pass 1 writes every row (no memset of the planes)
-      uint4* dst = reinterpret_cast<uint4*>(a.sp + ((size_t)(gz * d1 + gy) * nseg + tx) * kSP);
-      __stcg(dst, make_uint4(cnt[i][0] & vmask, cnt[i][1] & vmask, cnt[i][2] & vmask, cnt[i][3] & vmask));
-      __stcg(dst + 1, make_uint4(cnt[i][4] & vmask, cnt[i][5] & vmask, cnt[i][6] & vmask, cnt[i][7] & vmask));
-    }
-    if (!ch) continue;
-    nch += __popc(ch);
-    // next-tiling tiles of the rows z-1..z+1, y-1..y+1 relative to (tzb, tyb)
-#pragma unroll
-    for (int dz = -1; dz <= 1; ++dz) {
-      if (NDIM == 2 && dz) continue;
-      const int64_t z = gz + dz;
-      if (z < 0 || z >= d0) continue;
-      const int rz = (int)((z + (nt ? B::SZ : 0)) / G::TZ - tzb);
-#pragma unroll
-      for (int dy = -1; dy <= 1; ++dy) {
-        const int64_t y = gy + dy;
-        if (y < 0 || y >= d1) continue;
-        const int ry = (int)((y + (nt ? B::SY : 0)) / G::TY - tyb);
-        zy_mask |= 1u << (rz * 3 + ry);
-      }
-    }
-    xs |= 2u | (ch & 1u) | ((ch >> 31) << 2);  // bit 0: tx-1, 1: tx, 2: tx+1
+  for (int b = 0; b < kSP; ++b) ch |= cnt[b] ^ sp[b];
+  ch &= rin ? vmask : 0u;
+  if (SEEDED ? ch != 0u : rin) {  // pass 1 writes every row (no memset of the planes)
+    uint4* dst = reinterpret_cast<uint4*>(a.sp + ((size_t)(gz * d1 + gy) * nseg + tx) * kSP);
+    __stcg(dst, make_uint4(cnt[0] & vmask, cnt[1] & vmask, cnt[2] & vmask, cnt[3] & vmask));
+    __stcg(dst + 1, make_uint4(cnt[4] & vmask, cnt[5] & vmask, cnt[6] & vmask, cnt[7] & vmask));
   }
-  zy_mask = __reduce_or_sync(0xffffffffu, zy_mask);
-  xs = __reduce_or_sync(0xffffffffu, xs);
-  if (zy_mask) {
-    // lane k < 27 handles (rz, ry, rx) = k: mark, and append the fresh ones
+  const int nt = tiling ^ 1;
+  const int64_t nz0 = z0 - 1 + (nt ? G::SZ : 0), ny0 = y0 - 1 + (nt ? G::SY : 0);
+  const int64_t tzb = nz0 >= 0 ? nz0 / G::TZ : -1, tyb = ny0 >= 0 ? ny0 / G::TY : -1;  // next-tiling tile of (z0-1, y0-1)
+  // Only successors OUTSIDE this tile can have become unsatisfied (inside,
+  // the tile's fixpoint already accounts for every change): mark the
+  // next-tiling tiles holding the out-of-tile star neighbours of changed
+  // points.  m27 bit (rz * 9 + ry * 3 + rx): tile (tzb + rz, tyb + ry, tx + rx - 1).
+  uint32_t m27 = 0;
+  if (ch) {
+#pragma unroll
+    for (int j = 0; j < 2 * D; ++j) {
+      const int dz = slot_dz<NDIM>(j), dy = slot_dy<NDIM>(j), dx = slot_dx<NDIM>(j);
+      const int nz = lz + dz, ny = ly + dy;
+      const bool row_out = nz < 0 || nz >= G::TZ || ny < 0 || ny >= G::TY;
+      uint32_t xm;
+      if (row_out)
+        xm = dx == 0 ? 2u : dx > 0 ? (((ch & 0x7fffffffu) ? 2u : 0u) | ((ch >> 31) << 2)) : (((ch & 0xfffffffeu) ? 2u : 0u) | (ch & 1u));
+      else
+        xm = dx > 0 ? ((ch >> 31) << 2) : dx < 0 ? (ch & 1u) : 0u;
+      const int64_t z = gz + dz, y = gy + dy;
+      if (!xm || z < 0 || z >= d0 || y < 0 || y >= d1) continue;
+      const int rz = (int)((z + (nt ? G::SZ : 0)) / G::TZ - tzb);
+      const int ry = (int)((y + (nt ? G::SY : 0)) / G::TY - tyb);
+      m27 |= xm << (rz * 9 + ry * 3);
+    }
+  }
+  m27 = __reduce_or_sync(0xffffffffu, m27);
+  if (m27) {
+    // lane k < 27 marks tile k of the 3x3x3 neighbourhood; the fresh ones are appended
     const int rz = lane / 9, ry = (lane / 3) % 3, rx = lane % 3;
     bool fresh = false;
     uint32_t id = 0;
-    if (lane < 27 && ((zy_mask >> (rz * 3 + ry)) & 1u) && ((xs >> rx) & 1u)) {
-      const int64_t ntz = tzb + rz, nty = tyb + ry, ntx = (int64_t)tx + rx - 1;
-      if (ntz >= 0 && ntz < a.nt[nt][0] && nty >= 0 && nty < a.nt[nt][1] && ntx >= 0 && ntx < a.nt[nt][2]) {
-        id = (uint32_t)((ntz * a.nt[nt][1] + nty) * a.nt[nt][2] + ntx);
-        fresh = atomicOr(&a.act[nt][id], 1u) == 0u;
+    // (selects, not a.x[nt]: a runtime index into the parameter struct
+    // would copy it to local memory)
+    const uint32_t nz = nt ? a.nt[1][0] : a.nt[0][0], ny = nt ? a.nt[1][1] : a.nt[0][1], nx = a.nt[0][2];
+    uint32_t* act = nt ? a.act[1] : a.act[0];
+    uint32_t* lst = nt ? a.list[1] : a.list[0];
+    if (lane < 27 && ((m27 >> lane) & 1u)) {
+      const int64_t mtz = tzb + rz, mty = tyb + ry, mtx = (int64_t)tx + rx - 1;
+      if (mtz >= 0 && mtz < nz && mty >= 0 && mty < ny && mtx >= 0 && mtx < nx) {
+        id = (uint32_t)((mtz * ny + mty) * nx + mtx);
+        fresh = atomicOr(&act[id], 1u) == 0u;
       }
     }
     const uint32_t m = __ballot_sync(0xffffffffu, fresh);
@@ -366,16 +384,15 @@ __device__ __forceinline__ uint32_t tile_fix(const TileArgs& a, int tiling, uint
       uint32_t base = 0;
       if (lane == 0) base = atomicAdd(&a.ctr->tl_count[next_pass % 3], (uint32_t)__popc(m));
       base = __shfl_sync(0xffffffffu, base, 0);
-      if (fresh) a.list[nt][base + __popc(m & ((1u << lane) - 1u))] = id;
+      if (fresh) lst[base + __popc(m & ((1u << lane) - 1u))] = id;
     }
   }
-  return nch;
+  return (uint32_t)__popc(ch);
 }
 
 template <int NDIM>
 __global__ void __launch_bounds__(kTileThreads, LOPC_TILE_CTAS) k_tiles(TileArgs a) {
   namespace cg = cooperative_groups;
-  using G = Geo<NDIM>;
   __shared__ TileWarpSmem S[kTileWarps];
   cg::grid_group grid = cg::this_grid();
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -388,23 +405,29 @@ __global__ void __launch_bounds__(kTileThreads, LOPC_TILE_CTAS) k_tiles(TileArgs
     const int tiling = (q - 1) & 1;
     const uint32_t n = q == 1 ? a.ntiles[0] : *(volatile uint32_t*)&a.ctr->tl_count[q % 3];
     if (n == 0) break;
-    const uint32_t ntx = a.nt[tiling][2], ntxy = a.nt[tiling][1] * ntx;
-    for (;;) {
-      uint32_t t = 0;
-      if (lane == 0) t = atomicAdd(&a.ctr->tl_ticket[q % 3], 1u);
-      t = __shfl_sync(0xffffffffu, t, 0);
+    const uint32_t ntx = a.nt[0][2], ntxy = (tiling ? a.nt[1][1] : a.nt[0][1]) * ntx;
+    const uint32_t* lst = tiling ? a.list[1] : a.list[0];
+    uint32_t* act = tiling ? a.act[1] : a.act[0];
+    // pass 1: static round-robin over all tiles (uniform work); later
+    // passes: dynamic tickets over the active list
+    const uint32_t gw = blockIdx.x * kTileWarps + warp, nw = gridDim.x * kTileWarps;
+    for (uint32_t k = 0;; ++k) {
+      uint32_t t = gw + k * nw;
+      if (q > 1) {
+        if (lane == 0) t = atomicAdd(&a.ctr->tl_ticket[q % 3], 1u);
+        t = __shfl_sync(0xffffffffu, t, 0);
+      }
       if (t >= n) break;
       uint32_t id;
       if (q == 1) {
         id = t;
       } else {
-        id = __ldcg(&a.list[tiling][n - 1 - t]);  // reverse build order: alternate sweep direction
-        if (lane == 0) a.act[tiling][id] = 0u;     // may be marked again for pass q + 2
+        id = __ldcg(&lst[n - 1 - t]);  // reverse build order: alternate sweep direction
+        if (lane == 0) act[id] = 0u;    // may be marked again for pass q + 2
       }
       const uint32_t tz = id / ntxy, rem = id - tz * ntxy, ty = rem / ntx, tx = rem - ty * ntx;
-      uint32_t c = q == 1 ? tile_fix<NDIM, false>(a, tiling, tz, ty, tx, W, q + 1, my_max)
-                          : tile_fix<NDIM, true>(a, tiling, tz, ty, tx, W, q + 1, my_max);
-      my_changed += c;
+      my_changed += q == 1 ? tile_fix<NDIM, false>(a, tiling, tz, ty, tx, W, q + 1, my_max)
+                           : tile_fix<NDIM, true>(a, tiling, tz, ty, tx, W, q + 1, my_max);
     }
     if (tid == 0 && blockIdx.x == 0) {
       a.ctr->tl_count[(q + 2) % 3] = 0;
@@ -421,7 +444,6 @@ __global__ void __launch_bounds__(kTileThreads, LOPC_TILE_CTAS) k_tiles(TileArgs
   my_max = __reduce_max_sync(0xffffffffu, my_max);
   if (lane == 0 && cw) atomicAdd(&a.ctr->raised, (unsigned long long)cw);
   if (lane == 0 && my_max) atomicMax(&a.ctr->max_s, my_max);
-  (void)G::TZ;
 }
 
 // Subbin planes -> one u32 per point (the encoder's input, and repair_ex).
