@@ -164,6 +164,12 @@ void lopc_set_timing(int enable);
  * E_ARG for another value. */
 int lopc_set_repair_engine(int engine);
 
+/* Test switch (process-wide): force != 0 makes k_quant_flags and k_sweep
+ * use their int64 index builds on every grid (they are otherwise used only
+ * from N >= 2^31 - 2^24, e.g. the cfg5 slabs at N > 1), so the parity suite
+ * covers them on small grids.  Results are identical by construction. */
+int lopc_set_index64(int force);
+
 /* Message for a return code; lopc_last_error_string() adds CUDA / NCCL
  * detail of the calling thread's last failure. */
 const char* lopc_strerror(int code);

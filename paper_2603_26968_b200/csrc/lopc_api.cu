@@ -95,6 +95,9 @@ float inv32_of(double eps) {
   return (float)(1.0 / eps);
 }
 
+int g_force_i64 = 0;  // lopc_set_index64: test switch for the int64 index builds on small grids
+bool use_i32(const Shape& sh) { return !g_force_i64 && sh.n < (1ull << 31) - (1ull << 24); }
+
 struct CLayout {
   size_t ctr, bitmap, state, act0, act1, zero_end, plist, flags, s, sp, list0, list1, stage, sizes, off, stage_in,
       stage_out, total;
@@ -143,7 +146,7 @@ CLayout compress_layout(const Shape& s, bool host_in, bool host_out) {
   o += al(4 * L.tn[1]);
   L.zero_end = o;
   L.plist = o;
-  o += al(2 * (s.n < (1ull << 31) - (1ull << 24) ? 4 : 8) * s.n);
+  o += al(2 * (use_i32(s) ? 4 : 8) * s.n);  // worklist entries: the index width the kernels will use
   L.nseg = (s.d2 + 31) / 32;
   L.flags = o;
   o += al(4ull * s.d0 * s.d1 * L.nseg * (s.ndims == 3 ? Geo<3>::SW : Geo<2>::SW));
@@ -341,7 +344,6 @@ RepairArgs make_repair_args(const Shape& sh, const void* x, double eps, uint8_t*
   return ra;
 }
 
-bool use_i32(const Shape& sh) { return sh.n < (1ull << 31) - (1ull << 24); }
 
 // TMA tensor map of x for the halo-box loads of k_quant_flags (driver entry
 // point fetched at run time: no libcuda link dependency).  Returns false when
@@ -556,6 +558,11 @@ const char* lopc_strerror(int code) {
 const char* lopc_last_error_string(void) { return g_errmsg; }
 
 void lopc_set_timing(int enable) { g_timing = enable; }
+
+int lopc_set_index64(int force) {
+  g_force_i64 = force != 0;
+  return LOPC_OK;
+}
 
 int lopc_set_repair_engine(int engine) {
   if (engine < 0 || engine > 2) return LOPC_E_ARG;

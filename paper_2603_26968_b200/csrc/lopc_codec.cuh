@@ -3,10 +3,15 @@
 // Bins: "the lossless portion of PFPL" (readings G17-G19):
 //   DIFFNB_k -> BIT_k -> RZE_1.
 // Subbins: the LC pipelines BIT_4 RZE_4 RZE_1 / BIT_8 RZE_8 RZE_1.
-// One CTA encodes one 16 KiB chunk of both streams; the chunk's
-// payload offset is the exclusive prefix of (bin_size + sub_size) over the
-// previous chunks, found by a decoupled look-back (a7), so every payload is
-// written once, at its final place.  Stream format: DESIGN.md §4.
+// k_encode<T, 1> encodes the bins and k_encode<T, 2> the subbins of one
+// 16 KiB chunk per CTA, into the chunk's 32 KiB staging slot; then
+// k_chunk_scan (decoupled look-back over the size table: the exclusive prefix
+// of bin_size + sub_size, a7) and k_place copy every payload to its final
+// place (so the stream bytes move twice: a per-chunk look-back inside the
+// encoder was measured slower).  With the tile engine the
+// subbin CTAs read the repaired subbins as bit planes and the escape bits of
+// the flags, not x; the bound self-check a4 runs in the bin CTAs.  Stream
+// format: DESIGN.md §4.
 //
 // Word buffers in shared memory use an XOR swizzle so that the 32x32 bit
 // transposes of BIT_k run bank-conflict-free.  u32 words (f32): the 16-byte
@@ -430,11 +435,16 @@ __device__ uint32_t rze_dec(const uint8_t* in, uint32_t in_len, uint32_t L, int 
   if (act) *act = wend;
   constexpr int MAXIT = 5;
   const int iters = (int)((uact + kCodecThreads - 1) / kCodecThreads);
-  uint32_t running = 0;
-  bool bad = false;
+  // All units' masks first, then ONE block scan of the per-iteration data
+  // counts packed into a u64 (13 bits for each of iterations 0-3: <= 4096;
+  // 12 bits for iteration 4, which covers units 1024..1087: <= 1024), instead
+  // of one scan (three block barriers) per 256 units.
+  uint32_t mm[MAXIT];
+  unsigned long long pk = 0;
 #pragma unroll
   for (int it = 0; it < MAXIT; ++it) {
-    if (it >= iters) break;
+    mm[it] = 0;
+    if (it >= iters) continue;
     const uint32_t u = (uint32_t)(it * kCodecThreads + tid);
     uint32_t m = 0;
     if (u < uact) {
@@ -453,10 +463,23 @@ __device__ uint32_t rze_dec(const uint8_t* in, uint32_t in_len, uint32_t L, int 
       m = lo | (hi << 8);
       if (16 * u + 16 > n) m &= (1u << (n - 16 * u)) - 1u;
     }
-    uint32_t tot;
-    uint32_t dr = running + block_scan_excl<uint32_t>((uint32_t)__popc(m), R.wsum, &tot);
-    running += tot;
-    if (doff + (uint32_t)g * running > in_len) bad = true;  // block-uniform
+    mm[it] = m;
+    pk += (unsigned long long)__popc(m) << (13 * it);
+  }
+  unsigned long long ptot;
+  const unsigned long long pex = block_scan_excl<unsigned long long>(pk, R.wsum64, &ptot);
+  const uint32_t running_all = (uint32_t)((ptot & 0x1fff) + ((ptot >> 13) & 0x1fff) + ((ptot >> 26) & 0x1fff) +
+                                          ((ptot >> 39) & 0x1fff) + (ptot >> 52));
+  const bool bad = doff + (uint32_t)g * running_all > in_len;  // block-uniform
+  uint32_t running = 0;
+#pragma unroll
+  for (int it = 0; it < MAXIT; ++it) {
+    if (it >= iters) break;
+    const uint32_t u = (uint32_t)(it * kCodecThreads + tid);
+    const uint32_t m = mm[it];
+    const uint32_t field = it < 4 ? 0x1fffu : 0xfffu;
+    uint32_t dr = running + (uint32_t)((pex >> (13 * it)) & field);
+    running += (uint32_t)((ptot >> (13 * it)) & field);
     if (!bad && g == 1 && u < uact) {
       const uint8_t* src = in + doff;
       uint8_t* dst = out + u * ub;
@@ -478,10 +501,10 @@ __device__ uint32_t rze_dec(const uint8_t* in, uint32_t in_len, uint32_t L, int 
         uint4* o4 = reinterpret_cast<uint4*>(out + u * ub);
         for (int q = 0; q < pu / 4; ++q) o4[q] = make_uint4(0, 0, 0, 0);
       }
-      const uint32_t mm = u < uact ? m : 0u;
-      for (uint32_t nzl = __ballot_sync(0xffffffffu, mm != 0); nzl; nzl &= nzl - 1) {
+      const uint32_t mv = u < uact ? m : 0u;
+      for (uint32_t nzl = __ballot_sync(0xffffffffu, mv != 0); nzl; nzl &= nzl - 1) {
         const int l = __ffs(nzl) - 1;
-        const uint32_t mu = __shfl_sync(0xffffffffu, mm, l), du = __shfl_sync(0xffffffffu, dr, l);
+        const uint32_t mu = __shfl_sync(0xffffffffu, mv, l), du = __shfl_sync(0xffffffffu, dr, l);
         const uint32_t uu = u - lane + l;
         if (lane < pu) {
           const int j = lane >> uwl, hh = lane & ((1 << uwl) - 1);
@@ -748,7 +771,74 @@ __device__ __forceinline__ void gather_group(const EncodeArgs& a, uint64_t row, 
   for (int b = 0; b < NPL; ++b) pl[b] = 0;
   esc = 0;
   const uint32_t d2 = (uint32_t)a.d2;
-  for (uint32_t o = 0; o < 32 && left > 0;) {
+  if ((d2 & 31) == 0) {
+    // rows are whole segments: the group IS segment (row * nseg + x / 32)
+    if (left == 0) return;
+    const size_t rs = (size_t)row * (size_t)a.nseg + (x >> 5);
+    if constexpr (NPL == 4) {
+      const uint4 v = __ldg(reinterpret_cast<const uint4*>(a.sp + rs * 8 + b0));
+      pl[0] = v.x, pl[1] = v.y, pl[2] = v.z, pl[3] = v.w;
+    } else {
+      const uint2 v = __ldg(reinterpret_cast<const uint2*>(a.sp + rs * 8 + b0));
+      pl[0] = v.x, pl[1] = v.y;
+    }
+    if (want_esc) esc = __ldg(a.flags + rs * (size_t)a.sw + a.esc_word);
+    return;  // (n is a multiple of 32 here: no partial group)
+  }
+  if (d2 >= 32) {
+    // at most three pieces (the rest of a segment, the row's end, the next
+    // row's start): every load is issued before any is used
+    uint32_t o[3], bit[3], m[3];
+    size_t rs[3];
+    bool on[3];
+    uint32_t oo = 0;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      on[k] = oo < 32 && left > 0;
+      const uint32_t sg = x >> 5, bt = x & 31;
+      uint32_t take = 32 - bt < 32 - oo ? 32 - bt : 32 - oo;
+      if (d2 - x < take) take = d2 - x;
+      if (left < take) take = (uint32_t)left;
+      if (!on[k]) take = 0;
+      o[k] = oo;
+      bit[k] = bt;
+      m[k] = take >= 32 ? 0xffffffffu : ((1u << take) - 1u);
+      rs[k] = (size_t)row * (size_t)a.nseg + sg;
+      oo += take;
+      left -= take;
+      x += take;
+      if (x == d2) {
+        x = 0;
+        ++row;
+      }
+    }
+    uint32_t w[3][NPL], e[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      e[k] = 0;
+#pragma unroll
+      for (int b = 0; b < NPL; ++b) w[k][b] = 0;
+      if (on[k]) {
+        if constexpr (NPL == 4) {
+          const uint4 v = __ldg(reinterpret_cast<const uint4*>(a.sp + rs[k] * 8 + b0));
+          w[k][0] = v.x, w[k][1] = v.y, w[k][2] = v.z, w[k][3] = v.w;
+        } else {
+          static_assert(NPL == 2, "2 or 4 planes per thread");
+          const uint2 v = __ldg(reinterpret_cast<const uint2*>(a.sp + rs[k] * 8 + b0));
+          w[k][0] = v.x, w[k][1] = v.y;
+        }
+        if (want_esc) e[k] = __ldg(a.flags + rs[k] * (size_t)a.sw + a.esc_word);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+#pragma unroll
+      for (int b = 0; b < NPL; ++b) pl[b] |= ((w[k][b] >> bit[k]) & m[k]) << o[k];
+      esc |= ((e[k] >> bit[k]) & m[k]) << o[k];
+    }
+    return;
+  }
+  for (uint32_t o = 0; o < 32 && left > 0;) {  // rows shorter than a segment: one piece per row
     const uint32_t seg = x >> 5, bit = x & 31;
     uint32_t take = 32 - bit < 32 - o ? 32 - bit : 32 - o;
     if (d2 - x < take) take = d2 - x;
@@ -760,7 +850,6 @@ __device__ __forceinline__ void gather_group(const EncodeArgs& a, uint64_t row, 
       const uint4 v = __ldg(reinterpret_cast<const uint4*>(a.sp + rs * 8 + b0));
       w[0] = v.x, w[1] = v.y, w[2] = v.z, w[3] = v.w;
     } else {
-      static_assert(NPL == 2, "2 or 4 planes per thread");
       const uint2 v = __ldg(reinterpret_cast<const uint2*>(a.sp + rs * 8 + b0));
       w[0] = v.x, w[1] = v.y;
     }
@@ -848,6 +937,8 @@ struct EncSmem {
   RzeScratch R;
   unsigned long long pm[2];                  // OR of the words (subbins) / plane mask of BIT
   uint32_t misc[4];
+  unsigned long long row0;                   // planes mode: (row, x) of the chunk's first element
+  uint32_t x0;
 };
 
 template <typename T, int ROLE>
@@ -881,6 +972,10 @@ __global__ void __launch_bounds__(kCodecThreads, ROLE == 2 ? LOPC_SUBS_CTAS : LO
   if (tid == 0) {
     sm.misc[1] = 0;  // OR over the chunk of the plane-nonzero masks
     sm.misc[2] = 0;  // any escape in the chunk
+    if (a.sp) {      // (row, x) of the chunk's first element: one 64-bit division per CTA
+      sm.row0 = e0 / a.d2;
+      sm.x0 = (uint32_t)(e0 - sm.row0 * a.d2);
+    }
   }
   __syncthreads();
   if (a.sp) {  // gather the chunk's subbin planes and escape bits (both roles)
@@ -890,8 +985,8 @@ __global__ void __launch_bounds__(kCodecThreads, ROLE == 2 ? LOPC_SUBS_CTAS : LO
     // per CTA, then 32-bit steps (rows of d2 < 2^32 points).
     constexpr int NPL = 8 * G / kCodecThreads;
     const int g = tid % G, b0 = (tid / G) * NPL;
-    const uint64_t r0 = e0 / a.d2;
-    const uint32_t xg = (uint32_t)(e0 - r0 * a.d2) + 32u * (uint32_t)g, d2 = (uint32_t)a.d2;
+    const uint64_t r0 = sm.row0;
+    const uint32_t xg = sm.x0 + 32u * (uint32_t)g, d2 = (uint32_t)a.d2;
     const uint32_t dr = xg / d2;
     const uint64_t i0 = e0 + 32ull * g;
     uint32_t pl[NPL], esc;

@@ -155,21 +155,30 @@ __device__ __forceinline__ void load_sp_row(const TileArgs& a, bool in, int64_t 
 // The level loop of one tile on NP bit planes: cnt = the new subbins (planes
 // >= NP zero).  Returns L = 1 + the highest non-empty level, or -1 when a
 // level reaches 2^NP - 1 (the count would not fit NP planes).
+//
+// L0 (seeded passes): no constraint of this tile is violated below level L0
+// (every change since its points were last evaluated raised a point from a
+// value >= L0 - 1, so only levels >= L0 of its successors can have moved):
+// Lev_L = Seed_L for L < L0, and the loop starts at L0 from Seed_{L0-1}.
+// first_new: the lowest level where Lev_L != Seed_L (0: nothing changed) —
+// the level hint this visit passes on with its marks.
 template <int NDIM, bool SEEDED, int NP>
 __device__ __forceinline__ int tile_levels(const uint32_t (&F)[2 * TG<NDIM>::D], const uint32_t (&sp)[kSP], uint32_t eL,
                                            uint32_t eR, uint32_t hL, uint32_t hR, int bi, int hbi, int lz, int ly,
-                                           TileWarpSmem& W, uint32_t (&cnt)[kSP], bool prof, int& first_new) {
+                                           TileWarpSmem& W, uint32_t (&cnt)[kSP], int L0, int& first_new) {
   using G = TG<NDIM>;
   constexpr int D = G::D;
   constexpr int JX = D;  // the -x slot (0,0,-1): weight 0, closed by xfill
   const int lane = threadIdx.x & 31;
   (void)lz;
   (void)ly;
-  // level words of the box: all 0 (pass 1's halo stays 0)
+  // level words of the box: Lev_0 = every point (s >= 0: the flags mask the
+  // arcs, so all-ones serves), the other buffer 0 (pass 1's halo stays 0)
+  const int Ls = SEEDED ? L0 : 1;
   for (int t = lane; t < G::NB; t += 32) {
-    W.lv[0][t] = 0;
+    W.lv[0][t] = 0xffffffffu;
     W.lv[1][t] = 0;
-    W.ed[0][t] = 0;
+    W.ed[0][t] = 3;
     W.ed[1][t] = 0;
   }
   __syncwarp();
@@ -178,8 +187,30 @@ __device__ __forceinline__ int tile_levels(const uint32_t (&F)[2 * TG<NDIM>::D],
   for (int b = 0; b < NP; ++b) spn[b] = sp[b];
 #pragma unroll
   for (int b = 0; b < kSP; ++b) cnt[b] = 0;
+  first_new = 0;
+  if (SEEDED && L0 > 1) {
+    // start from Seed_{L0-1}: level words and edge bits of the tile and halo
+    // rows at L0 - 1, and the counts min(seed, L0 - 1)
+    const uint32_t Lb = (uint32_t)(L0 - 1);
+    uint32_t* prv = W.lv[Lb & 1];
+    uint8_t* pE = W.ed[Lb & 1];
+    if (lane < G::NH) {
+      uint32_t hp[NP];
+#pragma unroll
+      for (int b = 0; b < NP; ++b) hp[b] = W.hp[b][lane];
+      const int hb = W.hidx[lane];
+      prv[hb] = planes_ge<NP>(hp, Lb);
+      pE[hb] = (uint8_t)((hL >= Lb) | ((hR >= Lb) << 1));
+    }
+    const uint32_t m = planes_ge<NP>(spn, Lb);
+    prv[bi] = m;
+    pE[bi] = (uint8_t)((eL >= Lb) | ((eR >= Lb) << 1));
+#pragma unroll
+    for (int b = 0; b < NP; ++b) cnt[b] = (m & (0u - ((Lb >> b) & 1u))) | (~m & spn[b]);
+    __syncwarp();
+  }
   uint32_t X = 0;
-  int L = 1;
+  int L = Ls;
   for (;; ++L) {
     uint32_t* cur = W.lv[L & 1];
     const uint32_t* prv = W.lv[(L - 1) & 1];
@@ -197,19 +228,23 @@ __device__ __forceinline__ int tile_levels(const uint32_t (&F)[2 * TG<NDIM>::D],
       cE[bi] = (uint8_t)((eL >= (uint32_t)L) | ((eR >= (uint32_t)L) << 1));
       __syncwarp();
     }
-    uint32_t pv = SEEDED ? planes_ge<NP>(spn, (uint32_t)L) : 0u;
+    const uint32_t seedL = SEEDED ? planes_ge<NP>(spn, (uint32_t)L) : 0u;
+    uint32_t pv = seedL;
 #pragma unroll
-    for (int j = 0; j < D; ++j) {
-      if (L == 1) {
-        pv |= F[j];  // from any predecessor (s >= 0) through a w = 1 arc
-      } else {
-        const int t = bi + slot_dz<NDIM>(j) * G::BY + slot_dy<NDIM>(j);
-        uint32_t v = prv[t];
-        if (slot_dx<NDIM>(j) > 0) v = (v >> 1) | (SEEDED ? ((uint32_t)(pE[t] >> 1) << 31) : 0u);
-        pv |= F[j] & v;
-      }
+    for (int j = 0; j < D; ++j) {  // +e slots: w = 1 arcs from Lev_{L-1}
+      const int t = bi + slot_dz<NDIM>(j) * G::BY + slot_dy<NDIM>(j);
+      uint32_t v = prv[t];
+      if (slot_dx<NDIM>(j) > 0) v = (v >> 1) | ((uint32_t)(pE[t] >> 1) << 31);
+      pv |= F[j] & v;
     }
     if (SEEDED) pv |= F[JX] & (uint32_t)(cE[bi] & 1u);  // -x neighbour x0-1 (halo) at level L
+    if (!SEEDED && L == 1) {  // pass 1: the halo is 0 at every level >= 1 (the Lev_0 buffer is reused for L = 2)
+      __syncwarp();
+      for (int t = lane; t < G::NB; t += 32) {
+        W.lv[0][t] = 0;
+        W.ed[0][t] = 0;
+      }
+    }
     const uint32_t P = pv;
     X = xfill(pv, F[JX]);
     // -e closure across rows (weight 0), Jacobi until stable
@@ -231,8 +266,7 @@ __device__ __forceinline__ int tile_levels(const uint32_t (&F)[2 * TG<NDIM>::D],
       if (!__any_sync(0xffffffffu, ch)) break;
     }
     if (!__any_sync(0xffffffffu, X != 0)) break;  // Lev_L empty: done
-    if (SEEDED && prof && first_new == 0 && __any_sync(0xffffffffu, X != planes_ge<NP>(spn, (uint32_t)L)))
-      first_new = L;  // diagnostic: the lowest level where Lev_L != Seed_L
+    if (SEEDED && first_new == 0 && __any_sync(0xffffffffu, X != seedL)) first_new = L;
     if (L == (1 << NP) - 1) return -1;            // the count would not fit NP planes
     uint32_t carry = X;  // bit-sliced count += Lev_L
 #pragma unroll
@@ -252,7 +286,7 @@ __device__ __forceinline__ int tile_levels(const uint32_t (&F)[2 * TG<NDIM>::D],
 // returns this lane's number of changed points.
 template <int NDIM, bool SEEDED>
 __device__ __forceinline__ uint32_t tile_fix(const TileArgs& a, int tiling, uint32_t tz, uint32_t ty, uint32_t tx,
-                                             TileWarpSmem& W, int next_pass, uint32_t& my_max) {
+                                             TileWarpSmem& W, int next_pass, uint32_t& my_max, uint32_t* mark) {
   using G = TG<NDIM>;
   constexpr int D = G::D;
   constexpr int SW = G::SW;
@@ -268,6 +302,11 @@ __device__ __forceinline__ uint32_t tile_fix(const TileArgs& a, int tiling, uint
   const int lz = lane / G::TY, ly = lane % G::TY, bi = G::idx(lz, ly);
   const int64_t gz = z0 + lz, gy = y0 + ly;
   const bool rin = gz >= 0 && gz < d0 && gy >= 0 && gy < d1;
+  // this tile's mark word (seeded passes): 256 - the lowest level that may
+  // have moved (all marks for this pass were made in the previous one),
+  // loaded beside the row loads; reset so the tile can be marked again for
+  // the pass after next
+  const uint32_t mw = (SEEDED && mark) ? __ldcg(mark) : 0u;
   uint32_t F[2 * D];
   {
     const uint4* seg = reinterpret_cast<const uint4*>(a.flags + ((size_t)(rin ? gz * d1 + gy : 0) * nseg + tx) * SW);
@@ -305,12 +344,13 @@ __device__ __forceinline__ uint32_t tile_fix(const TileArgs& a, int tiling, uint
 #pragma unroll
   for (int b = 4; b < kSP; ++b) big |= sp[b] | (SEEDED && lane < G::NH ? W.hp[b][lane] : 0u);
   big |= (eL | eR | hL | hR) >> 4;
+  const int lmin = mw ? 256 - (int)mw : 1;
+  if (SEEDED && mark && lane == 0) *mark = 0u;
   int L = 0, first_new = 0;
   if (!__any_sync(0xffffffffu, big != 0))
-    L = tile_levels<NDIM, SEEDED, 4>(F, sp, eL, eR, hL, hR, bi, hbi, lz, ly, W, cnt, a.prof != 0, first_new);
+    L = tile_levels<NDIM, SEEDED, 4>(F, sp, eL, eR, hL, hR, bi, hbi, lz, ly, W, cnt, lmin, first_new);
   if (L <= 0) {
-    first_new = 0;
-    L = tile_levels<NDIM, SEEDED, kSP>(F, sp, eL, eR, hL, hR, bi, hbi, lz, ly, W, cnt, a.prof != 0, first_new);
+    L = tile_levels<NDIM, SEEDED, kSP>(F, sp, eL, eR, hL, hR, bi, hbi, lz, ly, W, cnt, lmin, first_new);
     if (L < 0) {  // s would not fit 8 planes: the host re-runs on the u32 engine
       if (lane == 0) atomicOr(&a.ctr->err, kErrPlanes);
       L = kMaxPlaneLevel;
@@ -321,8 +361,8 @@ __device__ __forceinline__ uint32_t tile_fix(const TileArgs& a, int tiling, uint
   if (SEEDED && a.prof && lane == 0) {  // diagnostic (lopc_set_timing(2)): seeded visits, visits with a change,
     atomicAdd(&a.ctr->dense_cycles[0], 1ull);  // levels run, levels below the first changed one
     if (first_new) atomicAdd(&a.ctr->dense_cycles[1], 1ull);
-    atomicAdd(&a.ctr->dense_cycles[2], (unsigned long long)L);
-    atomicAdd(&a.ctr->dense_cycles[3], (unsigned long long)(first_new ? first_new - 1 : L));
+    atomicAdd(&a.ctr->dense_cycles[2], (unsigned long long)(L - lmin + 1));
+    atomicAdd(&a.ctr->dense_cycles[3], (unsigned long long)(first_new ? first_new - lmin : L - lmin + 1));
   }
 
   // changed points, write-back, marks for the next pass
@@ -376,7 +416,9 @@ __device__ __forceinline__ uint32_t tile_fix(const TileArgs& a, int tiling, uint
       const int64_t mtz = tzb + rz, mty = tyb + ry, mtx = (int64_t)tx + rx - 1;
       if (mtz >= 0 && mtz < nz && mty >= 0 && mty < ny && mtx >= 0 && mtx < nx) {
         id = (uint32_t)((mtz * ny + mty) * nx + mtx);
-        fresh = atomicOr(&act[id], 1u) == 0u;
+        // mark word 256 - (lowest level that may have moved): the next visit
+        // starts there (pass 1 changes everything from level 1)
+        fresh = atomicMax(&act[id], 256u - (uint32_t)(SEEDED ? first_new : 1)) == 0u;
       }
     }
     const uint32_t m = __ballot_sync(0xffffffffu, fresh);
@@ -409,25 +451,19 @@ __global__ void __launch_bounds__(kTileThreads, LOPC_TILE_CTAS) k_tiles(TileArgs
     const uint32_t* lst = tiling ? a.list[1] : a.list[0];
     uint32_t* act = tiling ? a.act[1] : a.act[0];
     // pass 1: static round-robin over all tiles (uniform work); later
-    // passes: dynamic tickets over the active list
+    // passes: dynamic tickets over the active list, the next ticket fetched
+    // while the current tile runs (its atomic round trip off the critical path)
     const uint32_t gw = blockIdx.x * kTileWarps + warp, nw = gridDim.x * kTileWarps;
+    uint32_t tnext = gw;
+    if (q > 1 && lane == 0) tnext = atomicAdd(&a.ctr->tl_ticket[q % 3], 1u);
     for (uint32_t k = 0;; ++k) {
-      uint32_t t = gw + k * nw;
-      if (q > 1) {
-        if (lane == 0) t = atomicAdd(&a.ctr->tl_ticket[q % 3], 1u);
-        t = __shfl_sync(0xffffffffu, t, 0);
-      }
+      uint32_t t = q > 1 ? __shfl_sync(0xffffffffu, tnext, 0) : gw + k * nw;
       if (t >= n) break;
-      uint32_t id;
-      if (q == 1) {
-        id = t;
-      } else {
-        id = __ldcg(&lst[n - 1 - t]);  // reverse build order: alternate sweep direction
-        if (lane == 0) act[id] = 0u;    // may be marked again for pass q + 2
-      }
+      if (q > 1 && lane == 0) tnext = atomicAdd(&a.ctr->tl_ticket[q % 3], 1u);
+      const uint32_t id = q == 1 ? t : __ldcg(&lst[n - 1 - t]);  // reverse build order: alternate sweep direction
       const uint32_t tz = id / ntxy, rem = id - tz * ntxy, ty = rem / ntx, tx = rem - ty * ntx;
-      my_changed += q == 1 ? tile_fix<NDIM, false>(a, tiling, tz, ty, tx, W, q + 1, my_max)
-                           : tile_fix<NDIM, true>(a, tiling, tz, ty, tx, W, q + 1, my_max);
+      my_changed += q == 1 ? tile_fix<NDIM, false>(a, tiling, tz, ty, tx, W, q + 1, my_max, nullptr)
+                           : tile_fix<NDIM, true>(a, tiling, tz, ty, tx, W, q + 1, my_max, act + id);
     }
     if (tid == 0 && blockIdx.x == 0) {
       a.ctr->tl_count[(q + 2) % 3] = 0;

@@ -256,6 +256,15 @@ def set_repair_engine(engine: int):
     _check(L.lopc_set_repair_engine(int(engine)), "lopc_set_repair_engine")
 
 
+def set_index64(force: bool):
+    """Force the int64 index builds of k_quant_flags / k_sweep (test switch)."""
+    L = load(False)
+    L.lopc_set_index64.argtypes = [C.c_int]
+    L.lopc_set_index64.restype = C.c_int
+    _check(L.lopc_set_index64(int(bool(force))), "lopc_set_index64")
+    _size_cache.clear()  # workspace sizes depend on the index width
+
+
 def last_stats() -> dict:
     st = Stats()
     load(False).lopc_last_stats(C.byref(st))
