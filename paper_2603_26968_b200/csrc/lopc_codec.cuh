@@ -68,6 +68,51 @@ __device__ __forceinline__ V block_scan_excl(V v, V* wsum, V* total) {
   return base + x - v;
 }
 
+// Two u64 exclusive scans in one pass (the same three block barriers);
+// wsum needs 2 * NT/32 entries.
+template <int NT = kCodecThreads>
+__device__ __forceinline__ void block_scan_excl2(unsigned long long& a, unsigned long long& b, unsigned long long* wsum,
+                                                 unsigned long long& ta, unsigned long long& tb) {
+  constexpr int NW = NT / 32;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  unsigned long long x = a, y = b;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned long long xo = __shfl_up_sync(0xffffffffu, x, o), yo = __shfl_up_sync(0xffffffffu, y, o);
+    if (lane >= o) {
+      x += xo;
+      y += yo;
+    }
+  }
+  if (lane == 31) {
+    wsum[w] = x;
+    wsum[NW + w] = y;
+  }
+  __syncthreads();
+  if (w == 0) {
+    unsigned long long t = lane < NW ? wsum[lane] : 0ull, u = lane < NW ? wsum[NW + lane] : 0ull;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned long long to = __shfl_up_sync(0xffffffffu, t, o), uo = __shfl_up_sync(0xffffffffu, u, o);
+      if (lane >= o) {
+        t += to;
+        u += uo;
+      }
+    }
+    if (lane < NW) {
+      wsum[lane] = t;
+      wsum[NW + lane] = u;
+    }
+  }
+  __syncthreads();
+  const unsigned long long ba = w ? wsum[w - 1] : 0ull, bb = w ? wsum[NW + w - 1] : 0ull;
+  ta = wsum[NW - 1];
+  tb = wsum[2 * NW - 1];
+  __syncthreads();
+  a = ba + x - a;
+  b = bb + y - b;
+}
+
 // OR-combine `v` over aligned groups of `lanes` lanes.
 __device__ __forceinline__ uint32_t group_or(uint32_t v, int lanes) {
   for (int o = 1; o < lanes; o <<= 1) v |= __shfl_xor_sync(0xffffffffu, v, o);
@@ -92,7 +137,7 @@ struct RzeScratch {
   uint8_t k1[288];   // K1
   uint8_t k2[48];    // K2
   uint32_t wsum[32];
-  unsigned long long wsum64[32];
+  unsigned long long wsum64[32];  // (block_scan_excl2 uses 2 * 8 entries)
   uint32_t info[8];
 };
 
@@ -226,9 +271,14 @@ __device__ uint32_t rze_enc(const uint8_t* in, uint32_t L, int g, uint8_t* out, 
   const int iters = (int)((uvis + kCodecThreads - 1) / kCodecThreads);
   if (top >= 1)  // B1 words past the visited units are zero
     for (uint32_t t = (uint32_t)iters * (kCodecThreads / 16) + tid; t < (units + 15) / 16; t += kCodecThreads) R.b1[t] = 0;
+  // All units' masks first, then ONE pass of two u64 block scans: the data
+  // counts (13 bits per iteration 0-3, <= 4096; 12 bits for iteration 4,
+  // units >= 1024: <= 1024) and the K0 counts (10 bits per iteration, <= 512).
+  unsigned long long pd = 0, pkc = 0;
 #pragma unroll
   for (int it = 0; it < MAXIT; ++it) {
-    if (it >= iters) break;
+    mk[it] = 0;
+    if (it >= iters) continue;
     const uint32_t u = (uint32_t)(it * kCodecThreads + tid);
     uint32_t m = 0, prevb = 0;
     if (u < uvis) {
@@ -239,15 +289,23 @@ __device__ uint32_t rze_enc(const uint8_t* in, uint32_t L, int g, uint8_t* out, 
     const uint32_t lo = m & 0xffu, hi = m >> 8;
     uint32_t b1 = 0;
     if (top >= 1 && u < uvis) b1 = (uint32_t)(lo != prevb) | ((uint32_t)(hi != lo && 2 * u + 1 < sz[0]) << 1);
-    uint32_t tot;
-    const uint32_t ex = block_scan_excl<uint32_t>((uint32_t)__popc(m) | ((uint32_t)__popc(b1) << 20), R.wsum, &tot);
+    pd += (unsigned long long)__popc(m) << (13 * it);
+    pkc += (unsigned long long)__popc(b1) << (10 * it);
     mk[it] = m | (b1 << 16);
-    rk[it] = running + ex;
-    running += tot;
     if (top >= 1) {
       const uint32_t w = group_or(b1 << (2 * (u & 15)), 16);
       if ((lane & 15) == 0 && u < units) R.b1[u >> 4] = w;  // zero past uvis
     }
+  }
+  unsigned long long td, tk;
+  block_scan_excl2(pd, pkc, R.wsum64, td, tk);
+#pragma unroll
+  for (int it = 0; it < MAXIT; ++it) {
+    if (it >= iters) break;
+    const uint32_t field = it < 4 ? 0x1fffu : 0xfffu;
+    const uint32_t ex = (uint32_t)((pd >> (13 * it)) & field) | ((uint32_t)((pkc >> (10 * it)) & 0x3ffu) << 20);
+    rk[it] = running + ex;
+    running += (uint32_t)((td >> (13 * it)) & field) | ((uint32_t)((tk >> (10 * it)) & 0x3ffu) << 20);
   }
   const uint32_t ndata = running & 0xfffffu, nk0 = running >> 20;
   __syncthreads();
