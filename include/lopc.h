@@ -170,6 +170,12 @@ int lopc_set_repair_engine(int engine);
  * covers them on small grids.  Results are identical by construction. */
 int lopc_set_index64(int force);
 
+/* Decoder (process-wide): 1 (default) = one CTA per chunk decodes both
+ * streams and reconstructs from its own shared memory (k_decode1); 2 = the
+ * two streams of a chunk in a 2-CTA cluster, reconstructing through
+ * distributed shared memory (k_decode).  Same output.  E_ARG otherwise. */
+int lopc_set_decoder(int decoder);
+
 /* Message for a return code; lopc_last_error_string() adds CUDA / NCCL
  * detail of the calling thread's last failure. */
 const char* lopc_strerror(int code);

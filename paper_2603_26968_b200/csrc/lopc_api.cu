@@ -99,8 +99,8 @@ int g_force_i64 = 0;  // lopc_set_index64: test switch for the int64 index build
 bool use_i32(const Shape& sh) { return !g_force_i64 && sh.n < (1ull << 31) - (1ull << 24); }
 
 struct CLayout {
-  size_t ctr, bitmap, state, act0, act1, zero_end, plist, flags, s, sp, list0, list1, stage, sizes, off, stage_in,
-      stage_out, total;
+  size_t ctr, bitmap, state, act0, act1, zero_end, plist, flags, s, sp, escb, list0, list1, stage, sizes, off,
+      stage_in, stage_out, total;
   uint64_t bmw, nseg;
   int ntz, nty, ntx;
   uint64_t ntiles;
@@ -154,6 +154,8 @@ CLayout compress_layout(const Shape& s, bool host_in, bool host_out) {
   o += al(4 * s.n);
   L.sp = o;  // subbin planes (k_tiles): 8 words per 32-point segment
   o += al(4ull * kSP * s.d0 * s.d1 * L.nseg);
+  L.escb = o;  // escape bits (k_quant_flags): one word per segment
+  o += al(4ull * s.d0 * s.d1 * L.nseg);
   L.list0 = o;
   o += al(4 * L.tn[0]);
   L.list1 = o;
@@ -188,6 +190,7 @@ struct DevInfo {
   cudaStream_t side2 = nullptr;            // host-I/O decompress: D2H of decoded ranges
   cudaEvent_t ev_in[4] = {}, ev_dec[4] = {}, ev_out = nullptr;
   int occ_sweep2 = 0, occ_sweep3 = 0, occ_sweep2w = 0, occ_sweep3w = 0, occ_decode = 0, occ_tiles2 = 0, occ_tiles3 = 0;
+  int occ_decode1 = 0;
   bool attrs = false;
 };
 // One per (host thread, device): created on the thread's first call on that
@@ -218,6 +221,8 @@ int dev_info(DevInfo*& out) {
     CK(cudaFuncSetAttribute(k_encode<double, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     CK(cudaFuncSetAttribute(k_encode<double, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     CK(cudaFuncSetAttribute(k_decode, cudaFuncAttributeMaxDynamicSharedMemorySize, dsmem));
+    CK(cudaFuncSetAttribute(k_decode1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(DecSmem1)));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_dev.occ_decode1, k_decode1, kCodecThreads, sizeof(DecSmem1)));
 #define QRA(TT, ND)                                                                                      \
   CK(cudaFuncSetAttribute(k_quant_flags<TT, ND, int32_t, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                           (int)quant_flags_smem<TT, ND, false>()));                                        \
@@ -245,6 +250,26 @@ int dev_info(DevInfo*& out) {
     g_dev.attrs = true;
   }
   out = &g_dev;
+  return LOPC_OK;
+}
+
+// a8: k_decode1 (one CTA per chunk, both streams; the default) or k_decode
+// (2-CTA clusters; LOPC_DECODER=2), persistent over `chunks` chunks.
+int g_decoder = -1;  // lopc_set_decoder; -1: LOPC_DECODER from the environment, else 1
+int launch_decode(const DevInfo* di, const DecodeArgs& da, uint64_t chunks, cudaStream_t st) {
+  if (g_decoder < 0) g_decoder = getenv("LOPC_DECODER") ? atoi(getenv("LOPC_DECODER")) : 1;
+  if (g_decoder == 2) {
+    unsigned grid = 2u * (unsigned)(di->occ_decode > 0 ? di->occ_decode : 1);
+    if (grid > 2 * chunks) grid = (unsigned)(2 * chunks);
+    if (grid < 2) grid = 2;
+    k_decode<<<grid, kCodecThreads, sizeof(DecSmem), st>>>(da);
+  } else {
+    uint64_t grid = (uint64_t)(di->occ_decode1 > 0 ? di->occ_decode1 : 1) * (uint64_t)di->sms;
+    if (grid > chunks) grid = chunks;
+    if (grid < 1) grid = 1;
+    k_decode1<<<(unsigned)grid, kCodecThreads, sizeof(DecSmem1), st>>>(da);
+  }
+  CK(cudaGetLastError());
   return LOPC_OK;
 }
 
@@ -318,6 +343,7 @@ RepairArgs make_repair_args(const Shape& sh, const void* x, double eps, uint8_t*
   RepairArgs ra{};
   ra.x = x;
   ra.flags = reinterpret_cast<uint32_t*>(ws + L.flags);
+  ra.escb = reinterpret_cast<uint32_t*>(ws + L.escb);
   ra.nseg = (int64_t)L.nseg;
   ra.s = reinterpret_cast<uint32_t*>(ws + L.s);
   ra.plist = ws + L.plist;
@@ -559,6 +585,12 @@ const char* lopc_last_error_string(void) { return g_errmsg; }
 
 void lopc_set_timing(int enable) { g_timing = enable; }
 
+int lopc_set_decoder(int decoder) {
+  if (decoder != 1 && decoder != 2) return LOPC_E_ARG;
+  g_decoder = decoder;
+  return LOPC_OK;
+}
+
 int lopc_set_index64(int force) {
   g_force_i64 = force != 0;
   return LOPC_OK;
@@ -703,12 +735,10 @@ int compress_impl(const void* in, int ndims, const uint64_t* dims, int dtype, do
   // repair fills the SMs; with subbin planes the bin CTAs also run a4, which
   // needs the repaired subbins.)
   if ((rc = run_repair(sh, x, eps, ws, L, st, tm, engine, false))) return rc;  // marks 3, 4
-  if (engine == kEngTiles) {  // the encoder reads the subbin planes and the flags' escape words
+  if (engine == kEngTiles) {  // the encoder reads the subbin planes and the escape bitmap
     ea.sp = reinterpret_cast<const uint32_t*>(ws + L.sp);
-    ea.flags = reinterpret_cast<const uint32_t*>(ws + L.flags);
+    ea.escb = reinterpret_cast<const uint32_t*>(ws + L.escb);
     ea.nseg = (int64_t)L.nseg;
-    ea.sw = sh.ndims == 3 ? Geo<3>::SW : Geo<2>::SW;
-    ea.esc_word = ea.sw - 2;
   }
   launch_encode(ea, sh.dtype == LOPC_F64, 1, (unsigned)sh.C, smem, st);
   launch_encode(ea, sh.dtype == LOPC_F64, 2, (unsigned)sh.C, smem, st);
@@ -982,10 +1012,7 @@ int lopc_decompress_ex(const void* in, size_t in_bytes, void* out, size_t out_ca
       da.ctr = reinterpret_cast<Counters*>(ws + o_ctr);
       da.slab = 1;
       da.given = hh;
-      unsigned grid = 2u * (unsigned)(di->occ_decode > 0 ? di->occ_decode : 1);
-      if (grid > 2 * (ce - cb)) grid = (unsigned)(2 * (ce - cb));
-      k_decode<<<grid, kCodecThreads, sizeof(DecSmem), di->side>>>(da);
-      CK(cudaGetLastError());
+      if ((rc = launch_decode(di, da, ce - cb, di->side))) return rc;
       CK(cudaEventRecord(di->ev_dec[i], di->side));
       CK(cudaStreamWaitEvent(di->side2, di->ev_dec[i], 0));
       const uint64_t e0 = cb * W, e1 = ce * W < hh.n ? ce * W : hh.n;
@@ -1032,10 +1059,7 @@ int lopc_decompress_ex(const void* in, size_t in_bytes, void* out, size_t out_ca
   da.state_cap = cmax;
   da.prof = g_timing >= 2;
   da.ctr = reinterpret_cast<Counters*>(ws + o_ctr);
-  unsigned grid = 2u * (unsigned)(di->occ_decode > 0 ? di->occ_decode : 1);
-  if (grid > 2 * cmax) grid = (unsigned)(2 * cmax);
-  k_decode<<<grid, kCodecThreads, sizeof(DecSmem), st>>>(da);
-  CK(cudaGetLastError());
+  if ((rc = launch_decode(di, da, cmax, st))) return rc;
   tm.mark();  // 3
   CK(cudaMemcpyAsync(hc, ws + o_ctr, sizeof(Counters), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));

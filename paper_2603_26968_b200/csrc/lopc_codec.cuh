@@ -808,13 +808,12 @@ struct EncodeArgs {
   float xlim32;  // the same bound as a float (f32 data)
   // Subbin planes (tile engine, lopc_tiles.cuh): 8 u32 per 32-point x-segment
   // (word b = bit b of the segment's 32 subbins); null: u32 subbins in s.
-  // With planes, the escape bits come from word esc_word of each flag
-  // segment (k_quant_flags) and the bound self-check a4 runs in the bin
+  // With planes, the escape bits come from the escape bitmap of
+  // k_quant_flags (one u32 per segment) and the bound self-check a4 runs in the bin
   // CTAs, which hold x and the bins already: the subbin CTAs read no x.
   const uint32_t* sp;
-  const uint32_t* flags;
+  const uint32_t* escb;  // escape bits, one u32 per segment (k_quant_flags)
   int64_t nseg;
-  int sw, esc_word;
 };
 
 // Subbin planes b0 .. b0+NPL-1 (and, with ESC, the escape bits) of the 32
@@ -840,7 +839,7 @@ __device__ __forceinline__ void gather_group(const EncodeArgs& a, uint64_t row, 
       const uint2 v = __ldg(reinterpret_cast<const uint2*>(a.sp + rs * 8 + b0));
       pl[0] = v.x, pl[1] = v.y;
     }
-    if (want_esc) esc = __ldg(a.flags + rs * (size_t)a.sw + a.esc_word);
+    if (want_esc) esc = __ldg(a.escb + rs);
     return;  // (n is a multiple of 32 here: no partial group)
   }
   if (d2 >= 32) {
@@ -885,7 +884,7 @@ __device__ __forceinline__ void gather_group(const EncodeArgs& a, uint64_t row, 
           const uint2 v = __ldg(reinterpret_cast<const uint2*>(a.sp + rs[k] * 8 + b0));
           w[k][0] = v.x, w[k][1] = v.y;
         }
-        if (want_esc) e[k] = __ldg(a.flags + rs[k] * (size_t)a.sw + a.esc_word);
+        if (want_esc) e[k] = __ldg(a.escb + rs[k]);
       }
     }
 #pragma unroll
@@ -913,7 +912,7 @@ __device__ __forceinline__ void gather_group(const EncodeArgs& a, uint64_t row, 
     }
 #pragma unroll
     for (int b = 0; b < NPL; ++b) pl[b] |= ((w[b] >> bit) & m) << o;
-    if (want_esc) esc |= ((__ldg(a.flags + rs * (size_t)a.sw + a.esc_word) >> bit) & m) << o;
+    if (want_esc) esc |= ((__ldg(a.escb + rs) >> bit) & m) << o;
     o += take;
     left -= take;
     x += take;
@@ -1048,7 +1047,7 @@ __global__ void __launch_bounds__(kCodecThreads, ROLE == 2 ? LOPC_SUBS_CTAS : LO
     const uint32_t dr = xg / d2;
     const uint64_t i0 = e0 + 32ull * g;
     uint32_t pl[NPL], esc;
-    gather_group<NPL>(a, r0 + dr, xg - dr * d2, i0 < a.n ? a.n - i0 : 0, b0, b0 == 0, pl, esc);
+    gather_group<NPL>(a, r0 + dr, xg - dr * d2, i0 < a.n ? a.n - i0 : 0, b0, SUBS && b0 == 0, pl, esc);
     uint32_t nzp = 0;
 #pragma unroll
     for (int b = 0; b < NPL; ++b) {
@@ -1585,14 +1584,17 @@ __device__ __forceinline__ void load_payload(const uint8_t* g, uint32_t len, uin
 }
 
 template <typename T>
-__device__ __noinline__ void decode_stream(const DecodeArgs& a, const uint8_t* p, uint32_t size, bool subs, DecSmem& sm) {
+__device__ __noinline__ void decode_stream(const DecodeArgs& a, const uint8_t* p, uint32_t size, bool subs, DecSmem& sm,
+                                           uint8_t* BX, uint8_t* BY) {
   using U = typename VT<T>::U;
   constexpr int K = VT<T>::K;
   constexpr int W = kChunkBytes / K;
   constexpr int PER = W / kCodecThreads;
-  // words: subbins in place in sm.Wd; bins out of place into sm.O (their
-  // payload there is dead once RZE^-1 has produced the planes in sm.Wd)
-  U* WD = reinterpret_cast<U*>(subs ? sm.Wd : sm.O);
+  // Buffers: bins: payload BX -> planes BY -> words BX (out of place; the
+  // payload is dead once RZE^-1 has produced the planes); subbins: payload
+  // BX -> RZE_1^-1 output BY -> planes BX -> words BX (in place).  The
+  // 2-CTA decode passes (O, Wd) for bins and (Wd, O) for subbins.
+  U* WD = reinterpret_cast<U*>(BX);
   const int tid = threadIdx.x;
   bool bad = false;
   PhaseClock pc;
@@ -1607,22 +1609,22 @@ __device__ __noinline__ void decode_stream(const DecodeArgs& a, const uint8_t* p
   constexpr uint32_t PB = W / 8;  // bytes per bit plane
   uint32_t act = kChunkBytes;     // planes past act / PB are zero (and not written)
   if (!subs) {
-    load_payload(p, size, sm.O);
+    load_payload(p, size, BX);
     __syncthreads();
-    const uint32_t used = rze_dec(sm.O, size, kChunkBytes, 1, sm.Wd, sm.R, PB, &act);
+    const uint32_t used = rze_dec(BX, size, kChunkBytes, 1, BY, sm.R, PB, &act);
     if (used == 0xffffffffu || pad4(used) != size) bad = true;
   } else {
-    load_payload(p, size, sm.Wd);
+    load_payload(p, size, BX);
     __syncthreads();
-    const uint32_t l1 = (uint32_t)sm.Wd[0] | ((uint32_t)sm.Wd[1] << 8);
+    const uint32_t l1 = (uint32_t)BX[0] | ((uint32_t)BX[1] << 8);
     const uint32_t l1max = kChunkBytes + kChunkBytes / K / 8 + 64 + 8;
     if (l1 > l1max || size < 2) bad = true;
     if (!bad) {
-      const uint32_t used = rze_dec(sm.Wd + 2, size - 2, l1, 1, sm.O, sm.R, 0, nullptr);
+      const uint32_t used = rze_dec(BX + 2, size - 2, l1, 1, BY, sm.R, 0, nullptr);
       if (used == 0xffffffffu || pad4(2 + used) != size) bad = true;
     }
     if (!bad) {
-      const uint32_t used2 = rze_dec(sm.O, l1, kChunkBytes, K, sm.Wd, sm.R, PB, &act);
+      const uint32_t used2 = rze_dec(BY, l1, kChunkBytes, K, BX, sm.R, PB, &act);
       if (used2 != l1) bad = true;
     }
   }
@@ -1636,9 +1638,9 @@ __device__ __noinline__ void decode_stream(const DecodeArgs& a, const uint8_t* p
     return;
   }
   if (subs)
-    bit_inverse_planes<U, true>(sm.Wd, sm.Wd, W, (int)(act / PB));
+    bit_inverse_planes<U, true>(BX, BX, W, (int)(act / PB));
   else
-    bit_inverse_planes<U, false>(sm.Wd, sm.O, W, (int)(act / PB));
+    bit_inverse_planes<U, false>(BY, BX, W, (int)(act / PB));
   pc.mark(a.ctr, 11);
   if (!subs) {  // NB^-1 + prefix sum (thread owns PER consecutive words)
     U d[PER];
@@ -1820,9 +1822,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kCodecThreads, LOPC_
     const uint32_t sz = a.table[2 * l + r];
     const uint8_t* p = a.base + a.off[l] + (r ? a.table[2 * l] : 0u);
     if (h.dtype == 0)
-      decode_stream<float>(a, p, sz, r != 0, sm);
+      decode_stream<float>(a, p, sz, r != 0, sm, r ? sm.Wd : sm.O, r ? sm.O : sm.Wd);
     else
-      decode_stream<double>(a, p, sz, r != 0, sm);
+      decode_stream<double>(a, p, sz, r != 0, sm, r ? sm.Wd : sm.O, r ? sm.O : sm.Wd);
     cl.sync();  // release/acquire: the partner's words are complete
     const uint64_t c = a.c_begin + l;
     const bool ok = !s0->bad && !s1->bad;
@@ -1850,6 +1852,63 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kCodecThreads, LOPC_
     }
   }
   cl.sync();  // no CTA leaves while its partner may still read its flags
+}
+
+// Single-CTA decode (alternative to the 2-CTA cluster of k_decode): one CTA
+// decodes both streams of a chunk — bins (payload O -> planes Wd -> words
+// O), then subbins (payload Wd -> RZE_1^-1 output T -> planes / words Wd) —
+// and reconstructs both halves from its own shared memory: no cluster
+// barriers, no DSMEM copy; 4 CTAs/SM of 52 KB.  Persistent: CTA b decodes
+// chunks b, b + gridDim.x, ...
+#ifndef LOPC_DEC1_CTAS
+#define LOPC_DEC1_CTAS 4
+#endif
+struct DecSmem1 {
+  DecSmem d;
+  alignas(16) uint8_t T[17408 + 128];
+};
+
+__global__ void __launch_bounds__(kCodecThreads, LOPC_DEC1_CTAS) k_decode1(DecodeArgs a) {
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  DecSmem1& S = *reinterpret_cast<DecSmem1*>(smem_raw);
+  DecSmem& sm = S.d;
+  const int tid = threadIdx.x;
+  const Hdr h = parse_header(a);
+  if (!h.ok) {
+    if (blockIdx.x == 0 && tid == 0) atomicOr(&a.ctr->err, h.err);
+    return;
+  }
+  if (h32_err(a)) return;  // k_chunk_scan flagged the table
+  const uint64_t ncnk = a.slab ? a.c_count : (uint64_t)h.C;
+  if (tid == 0) sm.bad = 0;
+  for (uint64_t l = blockIdx.x; l < ncnk; l += gridDim.x) {
+    __syncthreads();  // the previous chunk's reconstruct is done with the buffers
+    const uint32_t bs = a.table[2 * l], ss = a.table[2 * l + 1];
+    const uint8_t* p = a.base + a.off[l];
+    if (h.dtype == 0) {
+      decode_stream<float>(a, p, bs, false, sm, sm.O, sm.Wd);
+      decode_stream<float>(a, p + bs, ss, true, sm, sm.Wd, S.T);
+    } else {
+      decode_stream<double>(a, p, bs, false, sm, sm.O, sm.Wd);
+      decode_stream<double>(a, p + bs, ss, true, sm, sm.Wd, S.T);
+    }
+    __syncthreads();
+    if (sm.bad) return;  // block-uniform; the error flag is set
+    const uint64_t c = a.c_begin + l;
+    for (int r = 0; r < 2; ++r) {
+      if (tid == 0) {
+        sm.tmin = INT_MAX;
+        sm.tmax = INT_MIN;
+      }
+      __syncthreads();
+      // the f32 lo-key table in T (free once the subbins are words)
+      if (h.dtype == 0)
+        reconstruct_half<float>(a, h, (uint32_t)c, r, sm.O, 0, sm.Wd, 0, sm, reinterpret_cast<int32_t*>(S.T));
+      else
+        reconstruct_half<double>(a, h, (uint32_t)c, r, sm.O, 0, sm.Wd, 0, sm, reinterpret_cast<int32_t*>(S.T));
+      __syncthreads();
+    }
+  }
 }
 
 }  // namespace lopc

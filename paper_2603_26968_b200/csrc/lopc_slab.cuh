@@ -743,10 +743,7 @@ int lopc_decompress_slab(const void* hdr64_host, const void* local, size_t local
   da.given.C = C;
   da.given.ok = true;
   da.given.err = 0;
-  unsigned grid = 2u * (unsigned)(di->occ_decode > 0 ? di->occ_decode : 1);
-  if (grid > 2 * CL) grid = (unsigned)(2 * CL);
-  k_decode<<<grid, kCodecThreads, sizeof(DecSmem), st>>>(da);
-  CK(cudaGetLastError());
+  if ((rc = launch_decode(di, da, CL, st))) return rc;
   tm.mark();  // 2
   CK(cudaMemcpyAsync(hc, ws, sizeof(Counters), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));

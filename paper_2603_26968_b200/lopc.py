@@ -256,6 +256,14 @@ def set_repair_engine(engine: int):
     _check(L.lopc_set_repair_engine(int(engine)), "lopc_set_repair_engine")
 
 
+def set_decoder(decoder: int):
+    """1: one CTA per chunk (default); 2: 2-CTA clusters."""
+    L = load(False)
+    L.lopc_set_decoder.argtypes = [C.c_int]
+    L.lopc_set_decoder.restype = C.c_int
+    _check(L.lopc_set_decoder(int(decoder)), "lopc_set_decoder")
+
+
 def set_index64(force: bool):
     """Force the int64 index builds of k_quant_flags / k_sweep (test switch)."""
     L = load(False)

@@ -86,3 +86,31 @@ def test_tile_engine_plane_overflow_falls_back(ref, gpu):
     y = (1.0 - 1e-6 * np.arange(200)).astype(np.float32).reshape(1, 200)  # fits: stays on the tile engine
     assert gpu.compress(_t(y), 1.0).cpu().numpy().tobytes() == ref.compress(y, 1.0)
     assert gpu.last_stats()["max_subbin"] == 199
+
+
+@pytest.mark.parametrize("decoder", [1, 2])
+def test_decoders_equal_oracle(ref, gpu, decoder):
+    """Both decoders (one CTA per chunk; 2-CTA clusters) give the oracle's
+    bits on f32 / f64 fields with escapes, raw chunks and ragged tails, from
+    device and host streams; a truncated stream is E_CORRUPT for both."""
+    import torch
+
+    gpu.set_repair_engine(0)
+    gpu.set_decoder(decoder)
+    try:
+        fields = [CONFIGS["cfg2"].generate((20, 100, 100)), random_field((70, 300), "f64", "smooth", 3),
+                  random_field((9, 31, 77), "f32", "noise", 5) * np.float32(1e6)]
+        fields[1].ravel()[::97] = np.nan
+        for x in fields:
+            eps = eps_noa(x, 1e-3)
+            st = ref.compress(x, eps)
+            y = ref.decompress(st).tobytes()
+            dev = torch.from_numpy(np.frombuffer(st, np.uint8).copy()).cuda()
+            assert gpu.decompress(dev).cpu().numpy().tobytes() == y
+            host = torch.from_numpy(np.frombuffer(st, np.uint8).copy()).pin_memory()
+            out = torch.empty(x.shape, dtype=torch.float32 if x.dtype == np.float32 else torch.float64).pin_memory()
+            assert gpu.decompress(host, out=out).numpy().tobytes() == y
+            with pytest.raises(gpu.LopcError):
+                gpu.decompress(dev[:-4])
+    finally:
+        gpu.set_decoder(1)
