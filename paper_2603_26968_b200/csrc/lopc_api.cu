@@ -99,8 +99,8 @@ int g_force_i64 = 0;  // lopc_set_index64: test switch for the int64 index build
 bool use_i32(const Shape& sh) { return !g_force_i64 && sh.n < (1ull << 31) - (1ull << 24); }
 
 struct CLayout {
-  size_t ctr, bitmap, state, act0, act1, zero_end, plist, flags, s, sp, escb, list0, list1, stage, sizes, off,
-      stage_in, stage_out, total;
+  size_t ctr, bitmap, state, act0, act1, zero_end, plist, flags, s, sp, list0, list1, stage, sizes, off, stage_in,
+      stage_out, total;
   uint64_t bmw, nseg;
   int ntz, nty, ntx;
   uint64_t ntiles;
@@ -154,8 +154,6 @@ CLayout compress_layout(const Shape& s, bool host_in, bool host_out) {
   o += al(4 * s.n);
   L.sp = o;  // subbin planes (k_tiles): 8 words per 32-point segment
   o += al(4ull * kSP * s.d0 * s.d1 * L.nseg);
-  L.escb = o;  // escape bits (k_quant_flags): one word per segment
-  o += al(4ull * s.d0 * s.d1 * L.nseg);
   L.list0 = o;
   o += al(4 * L.tn[0]);
   L.list1 = o;
@@ -220,6 +218,8 @@ int dev_info(DevInfo*& out) {
     CK(cudaFuncSetAttribute(k_encode<float, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     CK(cudaFuncSetAttribute(k_encode<double, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     CK(cudaFuncSetAttribute(k_encode<double, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    CK(cudaFuncSetAttribute(k_encode_both<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    CK(cudaFuncSetAttribute(k_encode_both<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     CK(cudaFuncSetAttribute(k_decode, cudaFuncAttributeMaxDynamicSharedMemorySize, dsmem));
     CK(cudaFuncSetAttribute(k_decode1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(DecSmem1)));
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_dev.occ_decode1, k_decode1, kCodecThreads, sizeof(DecSmem1)));
@@ -343,7 +343,6 @@ RepairArgs make_repair_args(const Shape& sh, const void* x, double eps, uint8_t*
   RepairArgs ra{};
   ra.x = x;
   ra.flags = reinterpret_cast<uint32_t*>(ws + L.flags);
-  ra.escb = reinterpret_cast<uint32_t*>(ws + L.escb);
   ra.nseg = (int64_t)L.nseg;
   ra.s = reinterpret_cast<uint32_t*>(ws + L.s);
   ra.plist = ws + L.plist;
@@ -735,13 +734,30 @@ int compress_impl(const void* in, int ndims, const uint64_t* dims, int dtype, do
   // repair fills the SMs; with subbin planes the bin CTAs also run a4, which
   // needs the repaired subbins.)
   if ((rc = run_repair(sh, x, eps, ws, L, st, tm, engine, false))) return rc;  // marks 3, 4
-  if (engine == kEngTiles) {  // the encoder reads the subbin planes and the escape bitmap
+  if (engine == kEngTiles) {  // the encoder reads the subbin planes and the flags' escape words
     ea.sp = reinterpret_cast<const uint32_t*>(ws + L.sp);
-    ea.escb = reinterpret_cast<const uint32_t*>(ws + L.escb);
+    ea.flags = reinterpret_cast<const uint32_t*>(ws + L.flags);
     ea.nseg = (int64_t)L.nseg;
+    ea.sw = sh.ndims == 3 ? Geo<3>::SW : Geo<2>::SW;
   }
-  launch_encode(ea, sh.dtype == LOPC_F64, 1, (unsigned)sh.C, smem, st);
-  launch_encode(ea, sh.dtype == LOPC_F64, 2, (unsigned)sh.C, smem, st);
+  // Both roles in one interleaved grid (k_encode_both; the two roles are
+  // independent: both read only x / the repaired subbins).  LOPC_ENC_MODE=1:
+  // the two kernels one after the other; 2: on two streams.
+  static const int enc_mode = getenv("LOPC_ENC_MODE") ? atoi(getenv("LOPC_ENC_MODE")) : 3;
+  if (enc_mode == 1) {
+    launch_encode(ea, sh.dtype == LOPC_F64, 1, (unsigned)sh.C, smem, st);
+    launch_encode(ea, sh.dtype == LOPC_F64, 2, (unsigned)sh.C, smem, st);
+  } else if (enc_mode == 2) {
+    CK(cudaEventRecord(di->ev_fork, st));
+    CK(cudaStreamWaitEvent(di->side, di->ev_fork, 0));
+    launch_encode(ea, sh.dtype == LOPC_F64, 2, (unsigned)sh.C, smem, di->side);
+    launch_encode(ea, sh.dtype == LOPC_F64, 1, (unsigned)sh.C, smem, st);
+    CK(cudaGetLastError());
+    CK(cudaEventRecord(di->ev_join, di->side));
+    CK(cudaStreamWaitEvent(st, di->ev_join, 0));
+  } else {
+    launch_encode(ea, sh.dtype == LOPC_F64, 3, (unsigned)sh.C, smem, st);
+  }
   CK(cudaGetLastError());
   tm.mark();  // 5
   ScanArgs sa{};

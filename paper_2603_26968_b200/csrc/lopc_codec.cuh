@@ -808,12 +808,13 @@ struct EncodeArgs {
   float xlim32;  // the same bound as a float (f32 data)
   // Subbin planes (tile engine, lopc_tiles.cuh): 8 u32 per 32-point x-segment
   // (word b = bit b of the segment's 32 subbins); null: u32 subbins in s.
-  // With planes, the escape bits come from the escape bitmap of
-  // k_quant_flags (one u32 per segment) and the bound self-check a4 runs in the bin
+  // With planes, the escape bits come from word sw - 2 of each flag segment
+  // (k_quant_flags) and the bound self-check a4 runs in the bin
   // CTAs, which hold x and the bins already: the subbin CTAs read no x.
   const uint32_t* sp;
-  const uint32_t* escb;  // escape bits, one u32 per segment (k_quant_flags)
+  const uint32_t* flags;  // flag segments: word sw - 2 holds the escape bits (k_quant_flags)
   int64_t nseg;
+  int sw;
 };
 
 // Subbin planes b0 .. b0+NPL-1 (and, with ESC, the escape bits) of the 32
@@ -839,7 +840,7 @@ __device__ __forceinline__ void gather_group(const EncodeArgs& a, uint64_t row, 
       const uint2 v = __ldg(reinterpret_cast<const uint2*>(a.sp + rs * 8 + b0));
       pl[0] = v.x, pl[1] = v.y;
     }
-    if (want_esc) esc = __ldg(a.escb + rs);
+    if (want_esc) esc = __ldg(a.flags + rs * (size_t)a.sw + (a.sw - 2));
     return;  // (n is a multiple of 32 here: no partial group)
   }
   if (d2 >= 32) {
@@ -884,7 +885,7 @@ __device__ __forceinline__ void gather_group(const EncodeArgs& a, uint64_t row, 
           const uint2 v = __ldg(reinterpret_cast<const uint2*>(a.sp + rs[k] * 8 + b0));
           w[k][0] = v.x, w[k][1] = v.y;
         }
-        if (want_esc) e[k] = __ldg(a.escb + rs[k]);
+        if (want_esc) e[k] = __ldg(a.flags + rs[k] * (size_t)a.sw + (a.sw - 2));
       }
     }
 #pragma unroll
@@ -912,7 +913,7 @@ __device__ __forceinline__ void gather_group(const EncodeArgs& a, uint64_t row, 
     }
 #pragma unroll
     for (int b = 0; b < NPL; ++b) pl[b] |= ((w[b] >> bit) & m) << o;
-    if (want_esc) esc |= ((__ldg(a.escb + rs) >> bit) & m) << o;
+    if (want_esc) esc |= ((__ldg(a.flags + rs * (size_t)a.sw + (a.sw - 2)) >> bit) & m) << o;
     o += take;
     left -= take;
     x += take;
@@ -999,7 +1000,7 @@ struct EncSmem {
 };
 
 template <typename T, int ROLE>
-__global__ void __launch_bounds__(kCodecThreads, ROLE == 2 ? LOPC_SUBS_CTAS : LOPC_CODEC_CTAS) k_encode(EncodeArgs a) {
+__device__ __forceinline__ void encode_chunk_role(const EncodeArgs& a, const uint32_t c, uint8_t* smem_raw) {
   using U = typename VT<T>::U;
   using I = typename VT<T>::I;
   constexpr bool SUBS = ROLE == 2;
@@ -1007,12 +1008,10 @@ __global__ void __launch_bounds__(kCodecThreads, ROLE == 2 ? LOPC_SUBS_CTAS : LO
   constexpr int W = kChunkBytes / K;
   constexpr int PER = W / kCodecThreads;  // words per thread (16 f32, 8 f64)
   constexpr int PB = W / 8;               // bytes per bit plane
-  extern __shared__ __align__(16) uint8_t smem_raw[];
   EncSmem& sm = *reinterpret_cast<EncSmem*>(smem_raw);
   U* WD = reinterpret_cast<U*>(sm.Wd);
   uint16_t* Q = reinterpret_cast<uint16_t*>(sm.O);
   const int tid = threadIdx.x, lane = tid & 31;
-  const uint32_t c = blockIdx.x;
   PhaseClock pc;
   pc.start(a.prof);
   if (tid == 0) {
@@ -1310,9 +1309,37 @@ __global__ void __launch_bounds__(kCodecThreads, ROLE == 2 ? LOPC_SUBS_CTAS : LO
   pc.mark(a.ctr, 7);
 }
 
-// Host: one k_encode grid of C CTAs for one stream (role 1 bins, 2 subbins).
+template <typename T, int ROLE>
+__global__ void __launch_bounds__(kCodecThreads, ROLE == 2 ? LOPC_SUBS_CTAS : LOPC_CODEC_CTAS) k_encode(EncodeArgs a) {
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  encode_chunk_role<T, ROLE>(a, blockIdx.x, smem_raw);
+}
+
+// Both roles in one grid of 2C CTAs, interleaved (CTA 2c: the bins of chunk
+// c, CTA 2c + 1: its subbins), so every SM holds CTAs of both kinds: the bin
+// CTAs are issue-bound, the subbin CTAs barrier-bound, and the scheduler
+// fills one's stalls with the other's instructions.  (Two kernels on two
+// streams do not overlap: each fills the GPU until its own tail.)
+template <typename T>
+__global__ void __launch_bounds__(kCodecThreads, LOPC_SUBS_CTAS) k_encode_both(EncodeArgs a) {
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  if (blockIdx.x & 1)
+    encode_chunk_role<T, 2>(a, blockIdx.x >> 1, smem_raw);
+  else
+    encode_chunk_role<T, 1>(a, blockIdx.x >> 1, smem_raw);
+}
+
+// Host: one k_encode grid of C CTAs for one stream (role 1 bins, 2 subbins),
+// or role 3: both streams in one k_encode_both grid of 2C CTAs.
 inline void launch_encode(const EncodeArgs& ea, bool f64, int role, unsigned C, size_t smem, cudaStream_t st) {
   if (C == 0) return;
+  if (role == 3) {
+    if (!f64)
+      k_encode_both<float><<<2 * C, kCodecThreads, smem, st>>>(ea);
+    else
+      k_encode_both<double><<<2 * C, kCodecThreads, smem, st>>>(ea);
+    return;
+  }
   if (!f64)
     (role == 1 ? k_encode<float, 1> : k_encode<float, 2>)<<<C, kCodecThreads, smem, st>>>(ea);
   else

@@ -53,7 +53,7 @@ struct Geo<3> {
   static constexpr int HZ = TZ + 2, HY = TY + 2, HX = TX + 2;
   static constexpr int ZH = 1;
   static constexpr int D = 7;   // +e offsets (G2)
-  static constexpr int SW = 16; // words per 32-point flag segment (14 used)
+  static constexpr int SW = 16; // words per 32-point flag segment (14 slots, word 14 = escapes)
 };
 template <>
 struct Geo<2> {
@@ -61,7 +61,7 @@ struct Geo<2> {
   static constexpr int HZ = 1, HY = TY + 2, HX = TX + 2;
   static constexpr int ZH = 0;
   static constexpr int D = 3;
-  static constexpr int SW = 8;  // 6 used
+  static constexpr int SW = 8;  // 6 slots, word 6 = escapes
 };
 
 #ifndef LOPC_SWEEP_CTAS
@@ -184,7 +184,6 @@ enum : uint32_t {
 struct RepairArgs {
   const void* x;
   uint32_t* flags;    // bit-plane flags: segment (z, y, xs) at ((z*d1 + y)*nseg + xs)*SW
-  uint32_t* escb;     // escape bits, one u32 per segment (null: not written)
   uint32_t* s;
   void* plist;        // 2 x cap point indices (Idx-sized), worklists of passes >= 2
   uint32_t* bitmap;   // 2 x bmw words: per-point "already enqueued" bits, self-clearing
@@ -550,11 +549,12 @@ __global__ void __launch_bounds__(kRepairThreads, sizeof(T) == 4 ? LOPC_QF_CTAS 
       wv[j] = __ballot_sync(0xffffffffu, arc);
     }
     const Idx gz = z0 + lz, gy = y0 + ly;
-    // escape bits (non-regular in-grid points: NaN, +-Inf, |b| > BINMAX),
-    // one u32 per segment in a.escb: read by the subbin encoder in planes
-    // mode instead of x (4 B per 32 points, coalesced across segments)
-    const uint32_t escw = __ballot_sync(0xffffffffu, lok == kHigh && gz < d0 && gy < d1 && x0 + lane < d2);
-    if (lane == 0 && gz < d0 && gy < d1 && a.escb) a.escb[(size_t)(gz * d1 + gy) * (size_t)a.nseg + (size_t)tx] = escw;
+    // word SW-2 (otherwise padding): escape bits (non-regular in-grid points:
+    // NaN, +-Inf, |b| > BINMAX), read by the subbin encoder in planes mode
+    // instead of x.  (A separate bitmap of one u32 per segment was measured:
+    // the extra scattered 4-byte stores cost k_quant_flags 9 % on cfg3, more
+    // than the encoder's sector reads of this word save.)
+    wv[G::SW - 2] = __ballot_sync(0xffffffffu, lok == kHigh && gz < d0 && gy < d1 && x0 + lane < d2);
     if (lane == 0 && gz < d0 && gy < d1) {
       const Idx rb = (gz * d1 + gy) * d2 + x0;
       if (rb < (Idx)a.own_lo || rb + 32 > (Idx)a.own_hi) {
