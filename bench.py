@@ -46,7 +46,7 @@ WORKLOAD = {
 CFG5_PLANES = 256  # z-planes of 2048^2 per rank
 # per-kernel keys -> the kernel that runs them (single-GPU engine 0; the slab
 # mode's repair is k_sweep + k_ghost_inject)
-KERNEL_NAMES = {"quant_flags": "k_quant_flags", "sweep": "k_tiles", "encode": "k_encode_both", "place": "k_place",
+KERNEL_NAMES = {"quant_flags": "k_quant_flags", "sweep": "k_tiles", "encode": "k_encode", "place": "k_place",
                 "decode_scan": "k_chunk_scan", "decode": "k_decode"}
 
 

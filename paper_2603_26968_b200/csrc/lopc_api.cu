@@ -218,8 +218,6 @@ int dev_info(DevInfo*& out) {
     CK(cudaFuncSetAttribute(k_encode<float, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     CK(cudaFuncSetAttribute(k_encode<double, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     CK(cudaFuncSetAttribute(k_encode<double, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    CK(cudaFuncSetAttribute(k_encode_both<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    CK(cudaFuncSetAttribute(k_encode_both<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     CK(cudaFuncSetAttribute(k_decode, cudaFuncAttributeMaxDynamicSharedMemorySize, dsmem));
     CK(cudaFuncSetAttribute(k_decode1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(DecSmem1)));
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_dev.occ_decode1, k_decode1, kCodecThreads, sizeof(DecSmem1)));
@@ -740,14 +738,17 @@ int compress_impl(const void* in, int ndims, const uint64_t* dims, int dtype, do
     ea.nseg = (int64_t)L.nseg;
     ea.sw = sh.ndims == 3 ? Geo<3>::SW : Geo<2>::SW;
   }
-  // Both roles in one interleaved grid (k_encode_both; the two roles are
-  // independent: both read only x / the repaired subbins).  LOPC_ENC_MODE=1:
-  // the two kernels one after the other; 2: on two streams.
-  static const int enc_mode = getenv("LOPC_ENC_MODE") ? atoi(getenv("LOPC_ENC_MODE")) : 3;
-  if (enc_mode == 1) {
+  // The two roles are independent (both read only x / the repaired
+  // subbins): the subbin grid runs on the side stream beside the bin grid
+  // (their tails overlap: cfg2 encode 0.239 -> 0.225 ms; cfg3 within 1 %).
+  // One interleaved grid of both roles was measured much slower (cfg3 1.15
+  // -> 2.0 ms: two large role bodies in one kernel, sharing the SMs' caches).
+  // LOPC_ENC_SERIAL=1: the two grids one after the other on `st`.
+  static const bool enc_serial = getenv("LOPC_ENC_SERIAL") && atoi(getenv("LOPC_ENC_SERIAL")) == 1;
+  if (enc_serial) {
     launch_encode(ea, sh.dtype == LOPC_F64, 1, (unsigned)sh.C, smem, st);
     launch_encode(ea, sh.dtype == LOPC_F64, 2, (unsigned)sh.C, smem, st);
-  } else if (enc_mode == 2) {
+  } else {
     CK(cudaEventRecord(di->ev_fork, st));
     CK(cudaStreamWaitEvent(di->side, di->ev_fork, 0));
     launch_encode(ea, sh.dtype == LOPC_F64, 2, (unsigned)sh.C, smem, di->side);
@@ -755,8 +756,6 @@ int compress_impl(const void* in, int ndims, const uint64_t* dims, int dtype, do
     CK(cudaGetLastError());
     CK(cudaEventRecord(di->ev_join, di->side));
     CK(cudaStreamWaitEvent(st, di->ev_join, 0));
-  } else {
-    launch_encode(ea, sh.dtype == LOPC_F64, 3, (unsigned)sh.C, smem, st);
   }
   CK(cudaGetLastError());
   tm.mark();  // 5

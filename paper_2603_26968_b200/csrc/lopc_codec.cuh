@@ -1315,31 +1315,9 @@ __global__ void __launch_bounds__(kCodecThreads, ROLE == 2 ? LOPC_SUBS_CTAS : LO
   encode_chunk_role<T, ROLE>(a, blockIdx.x, smem_raw);
 }
 
-// Both roles in one grid of 2C CTAs, interleaved (CTA 2c: the bins of chunk
-// c, CTA 2c + 1: its subbins), so every SM holds CTAs of both kinds: the bin
-// CTAs are issue-bound, the subbin CTAs barrier-bound, and the scheduler
-// fills one's stalls with the other's instructions.  (Two kernels on two
-// streams do not overlap: each fills the GPU until its own tail.)
-template <typename T>
-__global__ void __launch_bounds__(kCodecThreads, LOPC_SUBS_CTAS) k_encode_both(EncodeArgs a) {
-  extern __shared__ __align__(16) uint8_t smem_raw[];
-  if (blockIdx.x & 1)
-    encode_chunk_role<T, 2>(a, blockIdx.x >> 1, smem_raw);
-  else
-    encode_chunk_role<T, 1>(a, blockIdx.x >> 1, smem_raw);
-}
-
-// Host: one k_encode grid of C CTAs for one stream (role 1 bins, 2 subbins),
-// or role 3: both streams in one k_encode_both grid of 2C CTAs.
+// Host: one k_encode grid of C CTAs for one stream (role 1 bins, 2 subbins).
 inline void launch_encode(const EncodeArgs& ea, bool f64, int role, unsigned C, size_t smem, cudaStream_t st) {
   if (C == 0) return;
-  if (role == 3) {
-    if (!f64)
-      k_encode_both<float><<<2 * C, kCodecThreads, smem, st>>>(ea);
-    else
-      k_encode_both<double><<<2 * C, kCodecThreads, smem, st>>>(ea);
-    return;
-  }
   if (!f64)
     (role == 1 ? k_encode<float, 1> : k_encode<float, 2>)<<<C, kCodecThreads, smem, st>>>(ea);
   else
