@@ -139,6 +139,7 @@ struct RzeScratch {
   uint32_t wsum[32];
   unsigned long long wsum64[32];  // (block_scan_excl2 uses 2 * 8 entries)
   uint32_t info[8];
+  uint32_t ud[256];  // g = 4 / 8: per unit, non-zero word mask | data rank << 16
 };
 
 __device__ __forceinline__ int rze_sizes(uint32_t n, uint32_t* sz) {
@@ -342,7 +343,6 @@ __device__ uint32_t rze_enc(const uint8_t* in, uint32_t L, int g, uint8_t* out, 
   __syncthreads();
   const uint32_t koff = R.info[0], doff = R.info[1], total = R.info[2];
   if (total <= limit) {
-    const int lane = tid & 31;
 #pragma unroll
     for (int it = 0; it < MAXIT; ++it) {
       if (it >= iters) break;
@@ -372,27 +372,31 @@ __device__ uint32_t rze_enc(const uint8_t* in, uint32_t L, int g, uint8_t* out, 
             if ((m >> j) & 1u) d[r++] = (uint8_t)(w4[j >> 2] >> (8 * (j & 3)));
           }
         }
-      } else {
-        // g = 4 / 8: one unit at a time per warp (units with data only), its
-        // 16 g-byte words spread over the lanes: conflict-free reads
-        const int uwl = g == 4 ? 0 : 1;  // log2(u32 per word)
-        const int pu = 16 << uwl;         // u32 per unit
-        const uint32_t* in32 = reinterpret_cast<const uint32_t*>(in);
-        for (uint32_t nzl = __ballot_sync(0xffffffffu, m != 0); nzl; nzl &= nzl - 1) {
-          const int l = __ffs(nzl) - 1;
-          const uint32_t mu = __shfl_sync(0xffffffffu, m, l), du = __shfl_sync(0xffffffffu, dr, l);
-          const uint32_t uu = u - lane + l;
-          if (lane < pu) {
-            const int j = lane >> uwl, hh = lane & ((1 << uwl) - 1);
-            if ((mu >> j) & 1u) {
-              const uint32_t w = in32[uu * pu + lane];
-              uint8_t* o = d + (size_t)(du + __popc(mu & ((1u << j) - 1u))) * g + 4 * hh;
-              o[0] = (uint8_t)w;
-              o[1] = (uint8_t)(w >> 8);
-              o[2] = (uint8_t)(w >> 16);
-              o[3] = (uint8_t)(w >> 24);
-            }
-          }
+      } else if (valid) {
+        R.ud[u] = m | (dr << 16);  // g = 4 / 8: units <= 256, data ranks < 2^13
+      }
+    }
+  }
+  if (g != 1) {
+    // g = 4 / 8: the non-zero words of the visited units are scattered one
+    // u32 per thread step over the whole block (the units with data cluster
+    // in the first bit planes; one unit per warp at a time left most warps
+    // idle at the closing barrier)
+    __syncthreads();
+    if (total <= limit) {
+      const int uwl = g == 4 ? 0 : 1;  // log2(u32 per word)
+      const uint32_t pu = 16u << uwl;   // u32 per unit
+      const uint32_t* in32 = reinterpret_cast<const uint32_t*>(in);
+      uint8_t* d = out + doff;
+      for (uint32_t q = tid; q < uvis * pu; q += kCodecThreads) {
+        const uint32_t e = R.ud[q >> (4 + uwl)], m = e & 0xffffu, j = (q & (pu - 1u)) >> uwl;
+        if ((m >> j) & 1u) {
+          const uint32_t w = in32[q];
+          uint8_t* o = d + (size_t)((e >> 16) + __popc(m & ((1u << j) - 1u))) * g + 4 * (q & (uint32_t)((1 << uwl) - 1));
+          o[0] = (uint8_t)w;
+          o[1] = (uint8_t)(w >> 8);
+          o[2] = (uint8_t)(w >> 16);
+          o[3] = (uint8_t)(w >> 24);
         }
       }
     }
@@ -546,33 +550,36 @@ __device__ uint32_t rze_dec(const uint8_t* in, uint32_t in_len, uint32_t L, int 
       for (int j = 0; j < 16; ++j)
         if ((m >> j) & 1u) w4[j >> 2] |= (uint32_t)src[dr++] << (8 * (j & 3));
       *reinterpret_cast<uint4*>(dst) = make_uint4(w4[0], w4[1], w4[2], w4[3]);
-    } else if (!bad && g != 1) {
-      // g = 4 / 8: units without data are zeroed by their thread; units with
-      // data are written one at a time per warp, their words spread over the
-      // lanes (conflict-free)
-      const int lane = tid & 31;
-      const int uwl = g == 4 ? 0 : 1;
-      const int pu = 16 << uwl;
+    } else if (!bad && g != 1 && u < uact) {
+      R.ud[u] = m | (dr << 16);  // g = 4 / 8: units <= 256, data ranks < 2^13
+    }
+  }
+  if (g != 1) {
+    // g = 4 / 8: the active units' words are rebuilt 16 bytes per thread
+    // step over the whole block (the units with data cluster in the first
+    // bit planes; one unit per warp at a time left most warps idle at the
+    // closing barrier)
+    __syncthreads();
+    if (!bad) {
+      const int uwl = g == 4 ? 0 : 1;      // log2(u32 per word)
+      const uint32_t q4 = 4u << uwl;       // 16-byte vectors per unit
       const uint8_t* src = in + doff;
-      uint32_t* out32 = reinterpret_cast<uint32_t*>(out);
-      if (u < uact && m == 0) {
-        uint4* o4 = reinterpret_cast<uint4*>(out + u * ub);
-        for (int q = 0; q < pu / 4; ++q) o4[q] = make_uint4(0, 0, 0, 0);
-      }
-      const uint32_t mv = u < uact ? m : 0u;
-      for (uint32_t nzl = __ballot_sync(0xffffffffu, mv != 0); nzl; nzl &= nzl - 1) {
-        const int l = __ffs(nzl) - 1;
-        const uint32_t mu = __shfl_sync(0xffffffffu, mv, l), du = __shfl_sync(0xffffffffu, dr, l);
-        const uint32_t uu = u - lane + l;
-        if (lane < pu) {
-          const int j = lane >> uwl, hh = lane & ((1 << uwl) - 1);
-          uint32_t v = 0;
-          if ((mu >> j) & 1u) {
-            const uint8_t* b = src + (size_t)(du + __popc(mu & ((1u << j) - 1u))) * g + 4 * hh;
-            v = (uint32_t)b[0] | ((uint32_t)b[1] << 8) | ((uint32_t)b[2] << 16) | ((uint32_t)b[3] << 24);
+      uint4* out4 = reinterpret_cast<uint4*>(out);
+      for (uint32_t q = tid; q < uact * q4; q += kCodecThreads) {
+        const uint32_t e = R.ud[q >> (2 + uwl)], m = e & 0xffffu, dr = e >> 16;
+        const uint32_t o = (q & (q4 - 1u)) * 4u;  // first u32 of the vector within its unit
+        uint32_t v[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const uint32_t j = (o + k) >> uwl, hh = (o + k) & (uint32_t)((1 << uwl) - 1);
+          v[k] = 0;
+          if ((m >> j) & 1u) {  // unaligned 4 bytes: two aligned words and a funnel shift
+            const uintptr_t ad = reinterpret_cast<uintptr_t>(src) + (uintptr_t)(dr + __popc(m & ((1u << j) - 1u))) * g + 4 * hh;
+            const uint32_t* w = reinterpret_cast<const uint32_t*>(ad & ~(uintptr_t)3);
+            v[k] = __funnelshift_r(w[0], w[1], (uint32_t)(ad & 3) * 8u);
           }
-          out32[uu * pu + lane] = v;
         }
+        out4[q] = make_uint4(v[0], v[1], v[2], v[3]);
       }
     }
   }
