@@ -219,8 +219,8 @@ int dev_info(DevInfo*& out) {
     CK(cudaFuncSetAttribute(k_encode<double, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     CK(cudaFuncSetAttribute(k_encode<double, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     CK(cudaFuncSetAttribute(k_decode, cudaFuncAttributeMaxDynamicSharedMemorySize, dsmem));
-    CK(cudaFuncSetAttribute(k_decode1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(DecSmem1)));
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_dev.occ_decode1, k_decode1, kCodecThreads, sizeof(DecSmem1)));
+    CK(cudaFuncSetAttribute(k_decode1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(DecSmem2)));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_dev.occ_decode1, k_decode1, kCodecThreads, sizeof(DecSmem2)));
 #define QRA(TT, ND)                                                                                      \
   CK(cudaFuncSetAttribute(k_quant_flags<TT, ND, int32_t, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                           (int)quant_flags_smem<TT, ND, false>()));                                        \
@@ -265,7 +265,7 @@ int launch_decode(const DevInfo* di, const DecodeArgs& da, uint64_t chunks, cuda
     uint64_t grid = (uint64_t)(di->occ_decode1 > 0 ? di->occ_decode1 : 1) * (uint64_t)di->sms;
     if (grid > chunks) grid = chunks;
     if (grid < 1) grid = 1;
-    k_decode1<<<(unsigned)grid, kCodecThreads, sizeof(DecSmem1), st>>>(da);
+    k_decode1<<<(unsigned)grid, kCodecThreads, sizeof(DecSmem2), st>>>(da);
   }
   CK(cudaGetLastError());
   return LOPC_OK;

@@ -221,7 +221,23 @@ __device__ __forceinline__ uint32_t level_up_warp(const uint8_t* bi, uint32_t si
 
 // one warp: rebuild bitmap level i from B_{i+1} (bn bytes) and K_i (kin):
 // B_i[t] = the last K byte selected at or before t (0 if none).  Returns |K_i|.
-__device__ __forceinline__ uint32_t level_down_warp(const uint8_t* bn, const uint8_t* kin, uint32_t si, uint8_t* bi) {
+__device__ __forceinline__ void pf_l1_bytes(const void* p) { asm volatile("prefetch.global.L1 [%0];" ::"l"(p)); }
+
+// Byte i of a decoder input: shared memory, or (GIN) the payload in global
+// memory read through L1 (the caller bounds i by the payload length).
+template <bool GIN>
+__device__ __forceinline__ uint32_t rd8(const uint8_t* p, uint32_t i) {
+  if constexpr (GIN)
+    return (uint32_t)__ldg(p + i);
+  else
+    return (uint32_t)p[i];
+}
+
+// (klim: bytes readable at kin — a corrupt payload may announce more K bytes
+// than it holds; with GIN those reads must not leave the payload)
+template <bool GIN = false>
+__device__ __forceinline__ uint32_t level_down_warp(const uint8_t* bn, const uint8_t* kin, uint32_t si, uint8_t* bi,
+                                                    uint32_t klim = 0xffffffffu) {
   const int lane = threadIdx.x & 31;
   uint32_t kcount = 0;
   for (uint32_t base = 0; base < si; base += 256) {
@@ -240,7 +256,7 @@ __device__ __forceinline__ uint32_t level_down_warp(const uint8_t* bn, const uin
     for (int k = 0; k < 8; ++k) {
       if (t0 + k < si) {
         r += (bits >> k) & 1u;
-        bi[t0 + k] = r ? kin[r - 1] : (uint8_t)0;
+        bi[t0 + k] = (uint8_t)(r && r - 1 < klim ? rd8<GIN>(kin, r - 1) : 0u);
       }
     }
     kcount += __shfl_sync(0xffffffffu, incl, 31);
@@ -415,6 +431,10 @@ __device__ uint32_t rze_enc(const uint8_t* in, uint32_t L, int g, uint8_t* out, 
 // it are all zero; only the bytes up to the next multiple of `align` after
 // them are written (the rest of `out` is left as it was) and *act returns
 // that length — the caller's bit planes past *act are zero.
+//
+// GIN: `in` is the payload in global memory (g = 1 only); every read stays
+// below in_len, whatever the payload announces.
+template <bool GIN = false>
 __device__ uint32_t rze_dec(const uint8_t* in, uint32_t in_len, uint32_t L, int g, uint8_t* out, RzeScratch& R,
                             uint32_t align, uint32_t* act) {
   const int tid = threadIdx.x;
@@ -432,16 +452,16 @@ __device__ uint32_t rze_dec(const uint8_t* in, uint32_t in_len, uint32_t L, int 
     uint8_t* b3 = reinterpret_cast<uint8_t*>(R.b3);
     if (ok && top >= 1) {
       uint8_t* bt = top == 1 ? b1 : (top == 2 ? b2 : b3);
-      if ((uint32_t)lane < sz[top]) bt[lane] = in[lane];
+      if ((uint32_t)lane < sz[top]) bt[lane] = (uint8_t)rd8<GIN>(in, lane);
       __syncwarp();
       if (top >= 3) {
-        const uint32_t k2n = level_down_warp(b3, in + pos, sz[2], b2);
+        const uint32_t k2n = level_down_warp<GIN>(b3, in + pos, sz[2], b2, in_len - pos);
         pos += k2n;
         ok = ok && pos <= in_len;
         __syncwarp();
       }
       if (ok && top >= 2) {
-        const uint32_t k1n = level_down_warp(b2, in + pos, sz[1], b1);
+        const uint32_t k1n = level_down_warp<GIN>(b2, in + pos, sz[1], b1, in_len - pos);
         pos += k1n;
         ok = ok && pos <= in_len;
         __syncwarp();
@@ -475,7 +495,7 @@ __device__ uint32_t rze_dec(const uint8_t* in, uint32_t in_len, uint32_t L, int 
       pos += carry;  // |K0|
       ok = ok && pos <= in_len;
       // B0[t] = B0[last] for t >= last; when that byte is 0, units >= ceil(last / 2) are zero
-      if (ok && align) uact = last < 0 ? 0u : (in[pos - 1] == 0 ? ((uint32_t)last + 1) / 2 : units);
+      if (ok && align) uact = last < 0 ? 0u : (rd8<GIN>(in, pos - 1) == 0 ? ((uint32_t)last + 1) / 2 : units);
       if (lane == 0) R.info[0] = koff;
     }
     if (lane == 0) {
@@ -513,14 +533,14 @@ __device__ uint32_t rze_dec(const uint8_t* in, uint32_t in_len, uint32_t L, int 
       uint32_t lo, hi;
       const uint32_t t0 = 2 * u, t1 = 2 * u + 1;
       if (top == 0) {
-        lo = t0 < sz[0] && t0 < in_len ? in[t0] : 0u;
-        hi = t1 < sz[0] && t1 < in_len ? in[t1] : 0u;
+        lo = t0 < sz[0] && t0 < in_len ? rd8<GIN>(in, t0) : 0u;
+        hi = t1 < sz[0] && t1 < in_len ? rd8<GIN>(in, t1) : 0u;
       } else {
         const uint32_t w0 = R.b1[t0 >> 5];
         const uint32_t r0 = R.pre1[t0 >> 5] + __popc(w0 & ((2u << (t0 & 31)) - 1u));
         const uint32_t r1 = r0 + ((w0 >> (t1 & 31)) & 1u);  // t0, t1 share a B1 word
-        lo = r0 ? in[koff + r0 - 1] : 0u;
-        hi = t1 < sz[0] ? (r1 ? in[koff + r1 - 1] : 0u) : 0u;
+        lo = r0 ? rd8<GIN>(in, koff + r0 - 1) : 0u;
+        hi = t1 < sz[0] ? (r1 ? rd8<GIN>(in, koff + r1 - 1) : 0u) : 0u;
       }
       m = lo | (hi << 8);
       if (16 * u + 16 > n) m &= (1u << (n - 16 * u)) - 1u;
@@ -548,13 +568,13 @@ __device__ uint32_t rze_dec(const uint8_t* in, uint32_t in_len, uint32_t L, int 
       uint32_t w4[4] = {0, 0, 0, 0};
 #pragma unroll
       for (int j = 0; j < 16; ++j)
-        if ((m >> j) & 1u) w4[j >> 2] |= (uint32_t)src[dr++] << (8 * (j & 3));
+        if ((m >> j) & 1u) w4[j >> 2] |= rd8<GIN>(src, dr++) << (8 * (j & 3));
       *reinterpret_cast<uint4*>(dst) = make_uint4(w4[0], w4[1], w4[2], w4[3]);
     } else if (!bad && g != 1 && u < uact) {
       R.ud[u] = m | (dr << 16);  // g = 4 / 8: units <= 256, data ranks < 2^13
     }
   }
-  if (g != 1) {
+  if (!GIN && g != 1) {
     // g = 4 / 8: the active units' words are rebuilt 16 bytes per thread
     // step over the whole block (the units with data cluster in the first
     // bit planes; one unit per warp at a time left most warps idle at the
@@ -1703,9 +1723,9 @@ __device__ __noinline__ void decode_stream(const DecodeArgs& a, const uint8_t* p
 // Thread t owns PER consecutive elements: lo(b) is computed only when the
 // bin changes from the thread's previous element (bins are locally
 // repetitive), and the values leave as 16-byte stores.
-template <typename T>
+template <typename T, typename SM>
 __device__ __forceinline__ void reconstruct_half(const DecodeArgs& a, const Hdr& h, uint32_t c, int r, const uint8_t* wb,
-                                                 int wb_off, const uint8_t* ws, int ws_off, DecSmem& sm,
+                                                 int wb_off, const uint8_t* ws, int ws_off, SM& sm,
                                                  int32_t* tab) {
   using U = typename VT<T>::U;
   using I = typename VT<T>::I;
@@ -1866,24 +1886,120 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kCodecThreads, LOPC_
   cl.sync();  // no CTA leaves while its partner may still read its flags
 }
 
-// Single-CTA decode (alternative to the 2-CTA cluster of k_decode): one CTA
-// decodes both streams of a chunk — bins (payload O -> planes Wd -> words
-// O), then subbins (payload Wd -> RZE_1^-1 output T -> planes / words Wd) —
-// and reconstructs both halves from its own shared memory: no cluster
-// barriers, no DSMEM copy; 4 CTAs/SM of 52 KB.  Persistent: CTA b decodes
-// chunks b, b + gridDim.x, ...
+// Single-CTA decode (the default; the 2-CTA cluster k_decode above is the
+// alternative, lopc_set_decoder(2)).  One CTA decodes both streams of a chunk
+// and reconstructs it from its own shared memory: no cluster barriers, no
+// DSMEM copy.  The payloads are read where they lie (global memory, through
+// L1; the next chunk's payload is prefetched into L1 while this one
+// decodes), so only two 16 KiB buffers are needed and 6 CTAs fit an SM:
+//   subbins: payload -> RZE_1^-1 -> C -> RZE_k^-1 -> planes A -> words A
+//   bins:    payload -> RZE_1^-1 -> planes C -> words C -> NB^-1 + prefix sum
+//   x^:      from the words in C (bins) and A (subbins); the f32 lo-key
+//            table of a half overwrites that half's bin words once every
+//            thread holds its elements (reconstruct_half).
+// Persistent: CTA b decodes chunks b, b + gridDim.x, ...
 #ifndef LOPC_DEC1_CTAS
-#define LOPC_DEC1_CTAS 4
+#define LOPC_DEC1_CTAS 6
 #endif
-struct DecSmem1 {
-  DecSmem d;
-  alignas(16) uint8_t T[17408 + 128];
+struct DecSmem2 {
+  alignas(16) uint8_t A[kChunkBytes + 64];  // subbins: planes -> words
+  alignas(16) uint8_t C[17408 + 128];       // subbins: RZE_1^-1 output; bins: planes -> words
+  RzeScratch R;
+  uint32_t bad;
+  int tmin, tmax;
 };
+
+// Raw chunk stream (size == kChunkBytes): the words as they are, swizzled.
+template <typename U>
+__device__ __forceinline__ void raw_words(const uint8_t* p, uint8_t* buf) {
+  constexpr int W = kChunkBytes / (int)sizeof(U);
+  const U* g = reinterpret_cast<const U*>(p);
+  U* wd = reinterpret_cast<U*>(buf);
+  for (int i = threadIdx.x; i < W; i += kCodecThreads) wd[swz<U>(i)] = g[i];
+}
+
+// Both streams of one chunk into words (bins in C, subbins in A).  Returns
+// false (block-uniform) for a corrupt payload.
+template <typename T>
+__device__ __noinline__ bool decode_chunk_g(const uint8_t* p, uint32_t bs, uint32_t ss, DecSmem2& sm) {
+  using U = typename VT<T>::U;
+  constexpr int K = VT<T>::K;
+  constexpr int W = kChunkBytes / K;
+  constexpr int PER = W / kCodecThreads;
+  constexpr uint32_t PB = W / 8;  // bytes per bit plane
+  const int tid = threadIdx.x;
+  const uint8_t* ps = p + bs;
+  // subbins
+  if (ss == kChunkBytes) {
+    raw_words<U>(ps, sm.A);
+  } else {
+    if (ss < 2) return false;
+    const uint32_t l1 = (uint32_t)__ldg(ps) | ((uint32_t)__ldg(ps + 1) << 8);
+    if (l1 > kChunkBytes + kChunkBytes / K / 8 + 64 + 8) return false;
+    const uint32_t used = rze_dec<true>(ps + 2, ss - 2, l1, 1, sm.C, sm.R, 0, nullptr);
+    if (used == 0xffffffffu || pad4(2 + used) != ss) return false;
+    uint32_t act = kChunkBytes;
+    const uint32_t used2 = rze_dec<false>(sm.C, l1, kChunkBytes, K, sm.A, sm.R, PB, &act);
+    if (used2 != l1) return false;
+    bit_inverse_planes<U, true>(sm.A, sm.A, W, (int)(act / PB));
+  }
+  // bins
+  if (bs == kChunkBytes) {
+    raw_words<U>(p, sm.C);
+    __syncthreads();
+    return true;
+  }
+  uint32_t act = kChunkBytes;
+  const uint32_t used = rze_dec<true>(p, bs, kChunkBytes, 1, sm.C, sm.R, PB, &act);
+  if (used == 0xffffffffu || pad4(used) != bs) return false;
+  bit_inverse_planes<U, true>(sm.C, sm.C, W, (int)(act / PB));
+  // NB^-1 + prefix sum (thread owns PER consecutive words)
+  U* WD = reinterpret_cast<U*>(sm.C);
+  U d[PER];
+  U run = 0;
+#pragma unroll
+  for (int v = 0; v < PER; ++v) {
+    U u;
+    if constexpr (sizeof(U) == 4) {
+      if (v % 4 == 0) {
+        const uint4 q = *reinterpret_cast<const uint4*>(&WD[swz<U>(tid * PER + v)]);
+        d[v] = q.x, d[v + 1] = q.y, d[v + 2] = q.z, d[v + 3] = q.w;
+      }
+      u = d[v];
+    } else {
+      u = WD[swz<U>(tid * PER + v)];
+    }
+    d[v] = (U)((u ^ nb_mask<U>()) - nb_mask<U>());
+    run += d[v];
+  }
+  U tot, ex;
+  if constexpr (sizeof(U) == 4)
+    ex = block_scan_excl<uint32_t>(run, sm.R.wsum, &tot);
+  else
+    ex = (U)block_scan_excl<unsigned long long>((unsigned long long)run, sm.R.wsum64,
+                                                 reinterpret_cast<unsigned long long*>(&tot));
+  U acc = ex;
+#pragma unroll
+  for (int v = 0; v < PER; ++v) {
+    acc += d[v];
+    d[v] = acc;
+  }
+#pragma unroll
+  for (int v = 0; v < PER; ++v) {
+    if constexpr (sizeof(U) == 4) {
+      if (v % 4 == 0)
+        *reinterpret_cast<uint4*>(&WD[swz<U>(tid * PER + v)]) = make_uint4(d[v], d[v + 1], d[v + 2], d[v + 3]);
+    } else {
+      WD[swz<U>(tid * PER + v)] = d[v];
+    }
+  }
+  __syncthreads();
+  return true;
+}
 
 __global__ void __launch_bounds__(kCodecThreads, LOPC_DEC1_CTAS) k_decode1(DecodeArgs a) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
-  DecSmem1& S = *reinterpret_cast<DecSmem1*>(smem_raw);
-  DecSmem& sm = S.d;
+  DecSmem2& sm = *reinterpret_cast<DecSmem2*>(smem_raw);
   const int tid = threadIdx.x;
   const Hdr h = parse_header(a);
   if (!h.ok) {
@@ -1892,20 +2008,25 @@ __global__ void __launch_bounds__(kCodecThreads, LOPC_DEC1_CTAS) k_decode1(Decod
   }
   if (h32_err(a)) return;  // k_chunk_scan flagged the table
   const uint64_t ncnk = a.slab ? a.c_count : (uint64_t)h.C;
-  if (tid == 0) sm.bad = 0;
   for (uint64_t l = blockIdx.x; l < ncnk; l += gridDim.x) {
-    __syncthreads();  // the previous chunk's reconstruct is done with the buffers
     const uint32_t bs = a.table[2 * l], ss = a.table[2 * l + 1];
     const uint8_t* p = a.base + a.off[l];
-    if (h.dtype == 0) {
-      decode_stream<float>(a, p, bs, false, sm, sm.O, sm.Wd);
-      decode_stream<float>(a, p + bs, ss, true, sm, sm.Wd, S.T);
-    } else {
-      decode_stream<double>(a, p, bs, false, sm, sm.O, sm.Wd);
-      decode_stream<double>(a, p + bs, ss, true, sm, sm.Wd, S.T);
+    {  // the next chunk's payload into L1 while this one decodes
+      const uint64_t ln = l + gridDim.x;
+      if (ln < ncnk) {
+        const uint8_t* pn = a.base + a.off[ln];
+        const uint32_t len = a.table[2 * ln] + a.table[2 * ln + 1];
+        const uintptr_t b0 = reinterpret_cast<uintptr_t>(pn) & ~(uintptr_t)127;
+        const uint32_t lines = (uint32_t)((reinterpret_cast<uintptr_t>(pn) + len + 127 - b0) >> 7);
+        for (uint32_t k = tid; k < lines; k += kCodecThreads) pf_l1_bytes(reinterpret_cast<const void*>(b0 + 128 * (uintptr_t)k));
+      }
     }
-    __syncthreads();
-    if (sm.bad) return;  // block-uniform; the error flag is set
+    __syncthreads();  // the previous chunk's reconstruct is done with the buffers
+    const bool ok = h.dtype == 0 ? decode_chunk_g<float>(p, bs, ss, sm) : decode_chunk_g<double>(p, bs, ss, sm);
+    if (!ok) {  // block-uniform
+      if (tid == 0) atomicOr(&a.ctr->err, kErrCorrupt);
+      return;
+    }
     const uint64_t c = a.c_begin + l;
     for (int r = 0; r < 2; ++r) {
       if (tid == 0) {
@@ -1913,11 +2034,14 @@ __global__ void __launch_bounds__(kCodecThreads, LOPC_DEC1_CTAS) k_decode1(Decod
         sm.tmax = INT_MIN;
       }
       __syncthreads();
-      // the f32 lo-key table in T (free once the subbins are words)
+      // the f32 lo-key table of half r over half r's bin words in C (loaded
+      // into registers before reconstruct_half's first barrier)
       if (h.dtype == 0)
-        reconstruct_half<float>(a, h, (uint32_t)c, r, sm.O, 0, sm.Wd, 0, sm, reinterpret_cast<int32_t*>(S.T));
+        reconstruct_half<float>(a, h, (uint32_t)c, r, sm.C, 0, sm.A, 0, sm,
+                                reinterpret_cast<int32_t*>(sm.C + r * (kChunkBytes / 2)));
       else
-        reconstruct_half<double>(a, h, (uint32_t)c, r, sm.O, 0, sm.Wd, 0, sm, reinterpret_cast<int32_t*>(S.T));
+        reconstruct_half<double>(a, h, (uint32_t)c, r, sm.C, 0, sm.A, 0, sm,
+                                 reinterpret_cast<int32_t*>(sm.C + r * (kChunkBytes / 2)));
       __syncthreads();
     }
   }
