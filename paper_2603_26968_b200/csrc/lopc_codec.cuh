@@ -183,6 +183,30 @@ __device__ __forceinline__ uint32_t nz_words8(const uint8_t* p, int g) {
   return m;
 }
 
+// Bits of an 8-bit (byte_mask) or 32-bit (word_mask) group starting at bit
+// `start` that lie below `size`.
+__device__ __forceinline__ uint32_t byte_mask(uint32_t size, uint32_t start) {
+  return start >= size ? 0u : (size - start >= 8 ? 0xffu : (1u << (size - start)) - 1u);
+}
+__device__ __forceinline__ uint32_t word_mask(uint32_t size, uint32_t start) {
+  return start >= size ? 0u : (size - start >= 32 ? 0xffffffffu : (1u << (size - start)) - 1u);
+}
+
+// Exclusive prefix over the warp of popc(bits) for 8-bit per-lane groups, by
+// eight independent ballots (no dependent shuffle chain); tot = the total.
+__device__ __forceinline__ uint32_t warp_prefix8(uint32_t bits, uint32_t& tot) {
+  const uint32_t lt = (1u << (threadIdx.x & 31)) - 1u;
+  uint32_t ex = 0;
+  tot = 0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const uint32_t b = __ballot_sync(0xffffffffu, (bits >> k) & 1u);
+    ex += __popc(b & lt);
+    tot += __popc(b);
+  }
+  return ex;
+}
+
 // one warp: next bitmap level.  bi: si bytes; writes B_{i+1} bytes to bn and
 // K_i (bytes of bi whose B_{i+1} bit is set) to kb; returns |K_i|.
 __device__ __forceinline__ uint32_t level_up_warp(const uint8_t* bi, uint32_t si, uint8_t* bn, uint8_t* kb) {
@@ -203,24 +227,16 @@ __device__ __forceinline__ uint32_t level_up_warp(const uint8_t* bi, uint32_t si
       }
       bn[t0 / 8] = (uint8_t)bits;
     }
-    const uint32_t c = __popc(bits);
-    uint32_t incl = c;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += y;
-    }
-    uint32_t pos = kcount + incl - c;
+    uint32_t tot;
+    uint32_t pos = kcount + warp_prefix8(bits, tot);
 #pragma unroll
     for (int k = 0; k < 8; ++k)
       if ((bits >> k) & 1u) kb[pos++] = bi[t0 + k];
-    kcount += __shfl_sync(0xffffffffu, incl, 31);
+    kcount += tot;
   }
   return kcount;
 }
 
-// one warp: rebuild bitmap level i from B_{i+1} (bn bytes) and K_i (kin):
-// B_i[t] = the last K byte selected at or before t (0 if none).  Returns |K_i|.
 __device__ __forceinline__ void pf_l1_bytes(const void* p) { asm volatile("prefetch.global.L1 [%0];" ::"l"(p)); }
 
 // Byte i of a decoder input: shared memory, or (GIN) the payload in global
@@ -233,35 +249,26 @@ __device__ __forceinline__ uint32_t rd8(const uint8_t* p, uint32_t i) {
     return (uint32_t)p[i];
 }
 
-// (klim: bytes readable at kin — a corrupt payload may announce more K bytes
-// than it holds; with GIN those reads must not leave the payload)
-template <bool GIN = false>
-__device__ __forceinline__ uint32_t level_down_warp(const uint8_t* bn, const uint8_t* kin, uint32_t si, uint8_t* bi,
-                                                    uint32_t klim = 0xffffffffu) {
-  const int lane = threadIdx.x & 31;
-  uint32_t kcount = 0;
-  for (uint32_t base = 0; base < si; base += 256) {
-    const uint32_t t0 = base + 8 * lane;
-    uint32_t bits = t0 < si ? (uint32_t)bn[t0 / 8] : 0u;
-    if (t0 < si && si - t0 < 8) bits &= (1u << (si - t0)) - 1u;
-    const uint32_t c = __popc(bits);
-    uint32_t incl = c;
+// One bitmap level down, in registers: lane l holds the 8 bits of level i+1
+// that select level-i bytes 8l..8l+7 (`bits`, masked to the level size) and
+// gets those bytes back: byte k = K_i[r - 1], r = the set bits at or before
+// it counting from kcount (0 when r = 0), i.e. B_i[t] is the last K byte
+// selected at or before t.  kcount += this block's |K_i|.  klim: bytes
+// readable at kin (a corrupt payload may announce more K bytes than it holds;
+// with GIN those reads must not leave the payload).
+template <bool GIN>
+__device__ __forceinline__ unsigned long long level_down_reg(uint32_t bits, const uint8_t* kin, uint32_t klim,
+                                                             uint32_t& kcount) {
+  uint32_t tot;
+  uint32_t r = kcount + warp_prefix8(bits, tot);
+  unsigned long long v = 0ull;
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += y;
-    }
-    uint32_t r = kcount + incl - c;
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      if (t0 + k < si) {
-        r += (bits >> k) & 1u;
-        bi[t0 + k] = (uint8_t)(r && r - 1 < klim ? rd8<GIN>(kin, r - 1) : 0u);
-      }
-    }
-    kcount += __shfl_sync(0xffffffffu, incl, 31);
+  for (int k = 0; k < 8; ++k) {
+    r += (bits >> k) & 1u;
+    v |= (unsigned long long)(r && r - 1 < klim ? rd8<GIN>(kin, r - 1) : 0u) << (8 * k);
   }
-  return kcount;
+  kcount += tot;
+  return v;
 }
 
 // RZE_g encode of `in` (shared, 16-byte aligned, L bytes, zero up to the next
@@ -443,51 +450,75 @@ __device__ uint32_t rze_dec(const uint8_t* in, uint32_t in_len, uint32_t L, int 
   const int top = rze_sizes(n, sz);
   const uint32_t units = (n + 15) / 16, ub = 16u * (uint32_t)g;
   if (tid < 32) {
+    // warp 0: the bitmap levels above B0, in registers (lane l holds the
+    // bytes 8l..8l+7 of a level; every prefix count is eight ballots, not a
+    // dependent shuffle chain), then the B1 words and their popcount prefix
     const int lane = tid;
     bool ok = sz[top] <= in_len;
     uint32_t pos = sz[top];
     uint32_t uact = units;
-    uint8_t* b1 = reinterpret_cast<uint8_t*>(R.b1);
-    uint8_t* b2 = reinterpret_cast<uint8_t*>(R.b2);
-    uint8_t* b3 = reinterpret_cast<uint8_t*>(R.b3);
     if (ok && top >= 1) {
-      uint8_t* bt = top == 1 ? b1 : (top == 2 ? b2 : b3);
-      if ((uint32_t)lane < sz[top]) bt[lane] = (uint8_t)rd8<GIN>(in, lane);
-      __syncwarp();
-      if (top >= 3) {
-        const uint32_t k2n = level_down_warp<GIN>(b3, in + pos, sz[2], b2, in_len - pos);
-        pos += k2n;
-        ok = ok && pos <= in_len;
-        __syncwarp();
+      unsigned long long b1v[2] = {0ull, 0ull};  // B1 bytes 8l.. (block 0) and 256 + 8l.. (block 1: sz1 > 256)
+      if (top == 1) {
+        if (lane == 0)
+          for (uint32_t k = 0; k < sz[1]; ++k) b1v[0] |= (unsigned long long)rd8<GIN>(in, k) << (8 * k);
+      } else {
+        unsigned long long b2v = 0ull;  // B2 bytes 8l..8l+7
+        if (top == 2) {
+          if (lane == 0)
+            for (uint32_t k = 0; k < sz[2]; ++k) b2v |= (unsigned long long)rd8<GIN>(in, k) << (8 * k);
+        } else {  // top == 3: B2 from B3 (the top bytes) and K2
+          const uint32_t bits = ((uint32_t)lane < sz[3] ? rd8<GIN>(in, lane) : 0u) & byte_mask(sz[2], 8u * lane);
+          uint32_t k2n = 0;
+          b2v = level_down_reg<GIN>(bits, in + pos, in_len - pos, k2n);
+          pos += k2n;
+          ok = ok && pos <= in_len;
+        }
+        if (ok) {
+          uint32_t k1n = 0;
+#pragma unroll
+          for (int blk = 0; blk < 2; ++blk) {
+            if (blk == 1 && sz[1] <= 256) break;
+            const uint32_t bi = 32u * blk + lane;  // the B2 byte that selects B1 bytes 8 bi .. 8 bi + 7
+            const unsigned long long src = __shfl_sync(0xffffffffu, b2v, (int)(bi >> 3));
+            const uint32_t bits = (uint32_t)(src >> (8 * (bi & 7))) & byte_mask(sz[1], 8u * bi);
+            b1v[blk] = level_down_reg<GIN>(bits, in + pos, in_len - pos, k1n);
+          }
+          pos += k1n;
+          ok = ok && pos <= in_len;
+        }
       }
-      if (ok && top >= 2) {
-        const uint32_t k1n = level_down_warp<GIN>(b2, in + pos, sz[1], b1, in_len - pos);
-        pos += k1n;
-        ok = ok && pos <= in_len;
-        __syncwarp();
-      }
-      // exclusive popcount prefix of B1 words, bits < sz0 only; last set bit
+      // B1 words 2 (32 blk + l), +1 (bits < sz0 only), their exclusive
+      // popcount prefix, and the last set bit
       const uint32_t nw1 = (sz[0] + 31) / 32;
       uint32_t carry = 0;
       int last = -1;
-      for (uint32_t base = 0; base < nw1; base += 32) {
-        const uint32_t w = base + lane;
-        uint32_t c = 0;
-        if (w < nw1) {
-          uint32_t word = (uint32_t)b1[4 * w] | ((uint32_t)b1[4 * w + 1] << 8) | ((uint32_t)b1[4 * w + 2] << 16) |
-                          ((uint32_t)b1[4 * w + 3] << 24);
-          if (sz[0] - 32 * w < 32) word &= (1u << (sz[0] - 32 * w)) - 1u;
-          R.b1[w] = word;
-          c = __popc(word);
-          if (word) last = (int)(32 * w) + 31 - __clz(word);
-        }
+#pragma unroll
+      for (int blk = 0; blk < 2; ++blk) {
+        if (blk == 1 && nw1 <= 64) break;
+        const uint32_t w = 2u * (32u * blk + lane);
+        const uint32_t w0 = (uint32_t)b1v[blk] & word_mask(sz[0], 32u * w);
+        const uint32_t w1 = (uint32_t)(b1v[blk] >> 32) & word_mask(sz[0], 32u * (w + 1));
+        const uint32_t c = __popc(w0) + __popc(w1);
         uint32_t incl = c;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
           const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
           if (lane >= o) incl += y;
         }
-        if (w < nw1) R.pre1[w] = carry + incl - c;
+        const uint32_t ex = carry + incl - c;
+        if (w < nw1) {
+          R.b1[w] = w0;
+          R.pre1[w] = ex;
+        }
+        if (w + 1 < nw1) {
+          R.b1[w + 1] = w1;
+          R.pre1[w + 1] = ex + __popc(w0);
+        }
+        if (w1)
+          last = (int)(32 * (w + 1)) + 31 - __clz(w1);
+        else if (w0)
+          last = (int)(32 * w) + 31 - __clz(w0);
         carry += __shfl_sync(0xffffffffu, incl, 31);
       }
       last = __reduce_max_sync(0xffffffffu, last);

@@ -389,11 +389,17 @@ __device__ __forceinline__ uint32_t tile_fix(const TileArgs& a, int tiling, uint
       const int dz = slot_dz<NDIM>(j), dy = slot_dy<NDIM>(j), dx = slot_dx<NDIM>(j);
       const int nz = lz + dz, ny = ly + dy;
       const bool row_out = nz < 0 || nz >= G::TZ || ny < 0 || ny >= G::TY;
+      // a changed p can only feed q = p + e_j if q -> p is not an arc: within
+      // a bin the arcs follow one total order (G4), so F_j(p) (the arc q -> p)
+      // rules p -> q out
+      const uint32_t cj = ch & ~F[j];
       uint32_t xm;
       if (row_out)
-        xm = dx == 0 ? 2u : dx > 0 ? (((ch & 0x7fffffffu) ? 2u : 0u) | ((ch >> 31) << 2)) : (((ch & 0xfffffffeu) ? 2u : 0u) | (ch & 1u));
+        xm = dx == 0 ? (cj ? 2u : 0u)
+                     : dx > 0 ? (((cj & 0x7fffffffu) ? 2u : 0u) | ((cj >> 31) << 2))
+                              : (((cj & 0xfffffffeu) ? 2u : 0u) | (cj & 1u));
       else
-        xm = dx > 0 ? ((ch >> 31) << 2) : dx < 0 ? (ch & 1u) : 0u;
+        xm = dx > 0 ? ((cj >> 31) << 2) : dx < 0 ? (cj & 1u) : 0u;
       const int64_t z = gz + dz, y = gy + dy;
       if (!xm || z < 0 || z >= d0 || y < 0 || y >= d1) continue;
       const int rz = (int)((z + (nt ? G::SZ : 0)) / G::TZ - tzb);
