@@ -464,10 +464,7 @@ int launch_sweep(const Shape& sh, RepairArgs& ra, const CLayout& L, cudaStream_t
 // a3 on the tile engine: one cooperative k_tiles launch (tile fixpoints over
 // alternating shifted tilings, subbin planes), then the planes widened to one
 // u32 per point for the encoder.
-int launch_tiles(const Shape& sh, const RepairArgs& ra, uint8_t* ws, const CLayout& L, cudaStream_t st, bool widen) {
-  DevInfo* di;
-  int rc = dev_info(di);
-  if (rc) return rc;
+TileArgs make_tile_args(const Shape& sh, const RepairArgs& ra, uint8_t* ws, const CLayout& L) {
   TileArgs ta{};
   ta.flags = ra.flags;
   ta.sp = reinterpret_cast<uint32_t*>(ws + L.sp);
@@ -485,6 +482,17 @@ int launch_tiles(const Shape& sh, const RepairArgs& ra, uint8_t* ws, const CLayo
   ta.ntiles[1] = (uint32_t)L.tn[1];
   ta.max_passes = 1 << 20;
   ta.prof = g_timing >= 2;
+  ta.q0 = 1;
+  return ta;
+}
+
+int launch_tiles(const Shape& sh, const RepairArgs& ra, uint8_t* ws, const CLayout& L, cudaStream_t st, bool widen,
+                 int q0 = 1) {
+  DevInfo* di;
+  int rc = dev_info(di);
+  if (rc) return rc;
+  TileArgs ta = make_tile_args(sh, ra, ws, L);
+  ta.q0 = q0;
   const int occ = sh.ndims == 3 ? di->occ_tiles3 : di->occ_tiles2;
   uint64_t grid = (uint64_t)occ * di->sms;
   const uint64_t need = (L.tn[1] + kTileWarps - 1) / kTileWarps;

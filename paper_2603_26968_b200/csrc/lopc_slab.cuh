@@ -7,11 +7,16 @@
 // [e0, e1) get no incoming arcs (k_quant_flags own range); those within H of
 // the range are ghosts whose subbins come from the neighbour ranks:
 //
-//   round 1  : k_quant_flags + k_sweep (dense + sparse), ghosts = 0
+//   round 1  : k_quant_flags + k_tiles (the single-GPU tile engine on the
+//              box), ghosts = 0
 //   round i+1: exchange the H boundary subbins with rank r-1 / r+1,
-//              k_ghost_inject (raise ghosts, enqueue their successors),
-//              sum of raised ghosts over ranks == 0 -> done,
-//              else k_sweep (sparse passes only)
+//              k_ghost_inject_tiles (raise ghosts in the planes, mark the
+//              tiles of their successors), sum of raised ghosts over
+//              ranks == 0 -> done, else k_tiles from the marked tiles (q0 = 2)
+//
+// A subbin above 8 planes (kErrPlanes; very long chains) makes every rank
+// re-run the call on the u32 engine (k_sweep dense + sparse passes, ghosts
+// injected by k_ghost_inject into its point worklist), same result.
 //
 // Every round only raises subbins toward the least fixpoint (all start at 0
 // and every raise is a valid relaxation), and at termination every owned
@@ -104,6 +109,7 @@ struct Slab {
   double eps;
   cudaStream_t st;
   RepairArgs ra;
+  bool tiles = true;  // repair engine: k_tiles (planes) or k_sweep (u32)
   uint64_t passes = 0, sparse_points = 0, rounds = 0;
 
   uint8_t* xbox() const { return ws + lay.xbox; }
@@ -131,17 +137,38 @@ struct Slab {
   uint8_t* recv_lo() const { return ws + lay.recv_lo; }
   uint8_t* recv_hi() const { return ws + lay.recv_hi; }
 
+  // the repair of round 1 (after k_quant_flags); with tiles the planes are
+  // widened to u32 after every launch (the halo exchange and the encoder
+  // read u32 subbins)
+  int repair1() {
+    if (tiles) return launch_tiles(geo.box, ra, ws, lay.L, st, true);
+    ra.skip_dense = 0;
+    return launch_sweep(geo.box, ra, lay.L, st);
+  }
   int round1() {
     int rc = launch_quant_flags(geo.box, ra, lay.L, st);
     if (rc) return rc;
-    ra.skip_dense = 0;
-    if ((rc = launch_sweep(geo.box, ra, lay.L, st))) return rc;
-    return LOPC_OK;
+    return repair1();
   }
   // after recv_lo/recv_hi hold the neighbours' boundary subbins
   int inject() {
-    CK(cudaMemsetAsync(&dctr()->list_count[0], 0, sizeof(dctr()->list_count), st));
     CK(cudaMemsetAsync(&dctr()->ghost_changed, 0, sizeof(uint64_t), st));
+    if (tiles) {
+      CK(cudaMemsetAsync(&dctr()->tl_count[0], 0, sizeof(dctr()->tl_count) + sizeof(dctr()->tl_ticket), st));
+      const TileArgs ta = make_tile_args(geo.box, ra, ws, lay.L);
+      auto gi = [&](const uint8_t* buf, uint64_t g0, uint64_t cnt) {
+        const unsigned gb = (unsigned)((cnt + 255) / 256 < 1184 ? (cnt + 255) / 256 : 1184);
+        if (geo.box.ndims == 3)
+          k_ghost_inject_tiles<3><<<gb, 256, 0, st>>>(ta, reinterpret_cast<const uint32_t*>(buf), (int64_t)g0, (int64_t)cnt);
+        else
+          k_ghost_inject_tiles<2><<<gb, 256, 0, st>>>(ta, reinterpret_cast<const uint32_t*>(buf), (int64_t)g0, (int64_t)cnt);
+      };
+      if (geo.glo) gi(recv_lo(), own_lo() - geo.glo, geo.glo);
+      if (geo.ghi) gi(recv_hi(), own_hi(), geo.ghi);
+      CK(cudaGetLastError());
+      return LOPC_OK;
+    }
+    CK(cudaMemsetAsync(&dctr()->list_count[0], 0, sizeof(dctr()->list_count), st));
     const bool i32 = use_i32(geo.box);
 #define GI(ND, IX, BUF, G0, CNT)                                                                                   \
   k_ghost_inject<ND, IX><<<(unsigned)((CNT + 255) / 256 < 1184 ? (CNT + 255) / 256 : 1184), 256, 0, st>>>(       \
@@ -165,6 +192,7 @@ struct Slab {
     return LOPC_OK;
   }
   int sweep_sparse() {
+    if (tiles) return launch_tiles(geo.box, ra, ws, lay.L, st, true, 2);
     ra.skip_dense = 1;
     return launch_sweep(geo.box, ra, lay.L, st);
   }
@@ -384,10 +412,12 @@ int lopc_write_header(void* hdr64, int ndims, const uint64_t* dims, int dtype, d
   return LOPC_OK;
 }
 
-int lopc_compress_slab(lopc_comm* comm, const void* in_slab, int ndims, const uint64_t* dims, int dtype, double eps,
+constexpr int kSlabRetryU32 = -1000;  // internal (never returned): a subbin above 8 planes on some rank
+
+int compress_slab_impl(lopc_comm* comm, const void* in_slab, int ndims, const uint64_t* dims, int dtype, double eps,
                        uint64_t e_begin, uint64_t e_end, void* out_local, size_t* out_local_bytes,
                        uint64_t* payload_offset, uint64_t* total_bytes, void* workspace, size_t workspace_bytes,
-                       void* stream) {
+                       void* stream, bool tiles) {
   if (!in_slab || !out_local || !out_local_bytes) return LOPC_E_ARG;
   Shape g;
   int rc = make_shape(ndims, dims, dtype, g);
@@ -435,6 +465,7 @@ int lopc_compress_slab(lopc_comm* comm, const void* in_slab, int ndims, const ui
   sl.x_own = in_slab;
   sl.eps = eps;
   sl.st = st;
+  sl.tiles = tiles;
   Timer tm;
   if ((rc = tm.init(st))) return rc;
   tm.mark();  // 0
@@ -466,17 +497,21 @@ int lopc_compress_slab(lopc_comm* comm, const void* in_slab, int ndims, const ui
   // unusable; the caller must tear the job down).
   int lrc = launch_quant_flags(G.box, sl.ra, sl.lay.L, st);
   tm.mark();  // 2
-  if (!lrc) lrc = launch_sweep(G.box, sl.ra, sl.lay.L, st);
+  if (!lrc) lrc = sl.repair1();
   if (!lrc && fault_injected(rank, 0)) lrc = LOPC_E_INTERNAL;
   uint64_t rounds = 1;
+  bool broke_on_failure = false;
   while (world > 1) {
     if ((rc = halo(reinterpret_cast<uint8_t*>(sl.s()), 4, ncclUint32))) return rc;
     if (!lrc) lrc = sl.inject();
     if (!lrc && fault_injected(rank, (int)rounds)) lrc = LOPC_E_INTERNAL;
     // round agreement: sum over ranks of (ghosts raised, local failures)
     uint64_t* sum = reinterpret_cast<uint64_t*>(sl.ws + sl.lay.ctr_sum);  // [0, 1] in, [2, 3] out
+    // (a device-side error bit of this rank, e.g. kErrPlanes, counts as a failure too)
     if (cudaMemcpyAsync(sum, &sl.dctr()->ghost_changed, 8, cudaMemcpyDeviceToDevice, st) != cudaSuccess ||
-        cudaMemsetAsync(sum + 1, 0, 8, st) != cudaSuccess || (lrc && cudaMemsetAsync(sum + 1, 1, 1, st) != cudaSuccess))
+        cudaMemsetAsync(sum + 1, 0, 8, st) != cudaSuccess ||
+        cudaMemcpyAsync(sum + 1, &sl.dctr()->err, 4, cudaMemcpyDeviceToDevice, st) != cudaSuccess ||
+        (lrc && cudaMemsetAsync(sum + 1, 1, 1, st) != cudaSuccess))
       lrc = lrc ? lrc : LOPC_E_CUDA;
     NK(g_nccl.AllReduce(sum, sum + 2, 2, ncclUint64, ncclSum, comm->comm, st));
     uint64_t hs[2] = {0, 1};
@@ -484,7 +519,9 @@ int lopc_compress_slab(lopc_comm* comm, const void* in_slab, int ndims, const ui
         cudaStreamSynchronize(st) != cudaSuccess)
       return set_cuda_error(cudaGetLastError(), "slab round agreement");
     if (hs[1] != 0) {  // some rank failed: everyone stops here
-      if (!lrc) lrc = LOPC_E_INTERNAL;  // the failing rank's own code wins in the final allgather
+      // (the failing rank's own code reaches every rank through the final
+      // allgather; a rank whose trouble is a device error bit reports it there)
+      broke_on_failure = true;
       break;
     }
     if (hs[0] == 0) break;
@@ -507,7 +544,9 @@ int lopc_compress_slab(lopc_comm* comm, const void* in_slab, int ndims, const ui
   uint32_t herr = hc->err;
   if (hc->passes >= (unsigned long long)sl.ra.max_passes && hc->list_count[(hc->passes + 1) % 3] != 0)
     herr |= kErrPassCap;  // a repair that did not converge is never encoded silently
-  const int local = lrc ? lrc : map_err(herr & ~kErrNoSpace);
+  int local = lrc ? lrc : map_err(herr & ~kErrNoSpace);
+  if (!lrc && (herr & kErrPlanes)) local = kSlabRetryU32;  // every rank re-runs on the u32 engine
+  if (!local && world > 1 && broke_on_failure) local = LOPC_E_INTERNAL;  // another rank failed
   uint64_t mine[2] = {hc->total_bytes, (uint64_t)err_rank(local)};
   std::vector<uint64_t> all(2 * world);
   if (world > 1) {
@@ -533,8 +572,11 @@ int lopc_compress_slab(lopc_comm* comm, const void* in_slab, int ndims, const ui
   g_stats.sub_bytes = hc->sub_bytes;
   g_stats.total_bytes = off;
   g_stats.inner_iters = rounds;  // slab mode: repair rounds (halo exchanges + 1)
-  g_stats.launches = (uint32_t)(2 + 3 * (rounds - 1) + 2 + 3);
+  // quant_flags + repair (+ widen), per further round: up to 2 injections +
+  // repair (+ widen); 2 encoder grids, scan, place
+  g_stats.launches = (uint32_t)((tiles ? 3 : 2) + (tiles ? 4 : 3) * (rounds - 1) + 2 + 2);
   const uint64_t need = 8 * G.C_local + mine[0];
+  if (worst == (uint64_t)-kSlabRetryU32) return kSlabRetryU32;
   if (worst) {
     if (-(int)worst == LOPC_E_NOSPACE) *out_local_bytes = need;  // lopc.h: NOSPACE reports the size needed
     return -(int)worst;
@@ -547,11 +589,26 @@ int lopc_compress_slab(lopc_comm* comm, const void* in_slab, int ndims, const ui
   return LOPC_OK;
 }
 
+int lopc_compress_slab(lopc_comm* comm, const void* in_slab, int ndims, const uint64_t* dims, int dtype, double eps,
+                       uint64_t e_begin, uint64_t e_end, void* out_local, size_t* out_local_bytes,
+                       uint64_t* payload_offset, uint64_t* total_bytes, void* workspace, size_t workspace_bytes,
+                       void* stream) {
+  const size_t cap = out_local_bytes ? *out_local_bytes : 0;
+  int rc = compress_slab_impl(comm, in_slab, ndims, dims, dtype, eps, e_begin, e_end, out_local, out_local_bytes,
+                              payload_offset, total_bytes, workspace, workspace_bytes, stream, g_engine == 0);
+  if (rc == kSlabRetryU32) {  // agreed by every rank: a subbin above 8 planes somewhere
+    *out_local_bytes = cap;
+    rc = compress_slab_impl(comm, in_slab, ndims, dims, dtype, eps, e_begin, e_end, out_local, out_local_bytes,
+                            payload_offset, total_bytes, workspace, workspace_bytes, stream, false);
+  }
+  return rc;
+}
+
 // Single-device test hook: the slab algorithm over `nslabs` ranges in one
 // call, with the halo exchanges done by device copies between the slabs.
 // Writes the whole stream.  Allocates its own workspaces (diagnostic only).
-int lopc_compress_slabs_local(const void* in, int ndims, const uint64_t* dims, int dtype, double eps, int nslabs,
-                              const uint64_t* bounds, void* out, size_t* out_bytes) {
+int compress_slabs_local_impl(const void* in, int ndims, const uint64_t* dims, int dtype, double eps, int nslabs,
+                              const uint64_t* bounds, void* out, size_t* out_bytes, bool tiles) {
   if (!in || !out || !out_bytes || !bounds || nslabs < 1) return LOPC_E_ARG;
   Shape g;
   int rc = make_shape(ndims, dims, dtype, g);
@@ -581,6 +638,7 @@ int lopc_compress_slabs_local(const void* in, int ndims, const uint64_t* dims, i
     sl[r].x_own = static_cast<const uint8_t*>(in) + g.k * bounds[r];
     sl[r].eps = eps;
     sl[r].st = st;
+    sl[r].tiles = tiles;
     if ((rc = sl[r].setup())) {
       cleanup();
       return rc;
@@ -614,11 +672,19 @@ int lopc_compress_slabs_local(const void* in, int ndims, const uint64_t* dims, i
     for (auto& a : sl)
       if ((rc = a.inject())) { cleanup(); return rc; }
     uint64_t changed = 0;
+    uint32_t errs = 0;
     for (auto& a : sl) {
       uint64_t v = 0;
+      uint32_t e = 0;
       CK(cudaMemcpyAsync(&v, &a.dctr()->ghost_changed, 8, cudaMemcpyDeviceToHost, st));
+      CK(cudaMemcpyAsync(&e, &a.dctr()->err, 4, cudaMemcpyDeviceToHost, st));
       CK(cudaStreamSynchronize(st));
       changed += v;
+      errs |= e;
+    }
+    if (errs & kErrPlanes) {
+      cleanup();
+      return kSlabRetryU32;
     }
     if (!changed) break;
     for (auto& a : sl)
@@ -639,6 +705,10 @@ int lopc_compress_slabs_local(const void* in, int ndims, const uint64_t* dims, i
     CK(cudaMemcpyAsync(hc, sl[r].dctr(), sizeof(Counters), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     pay[r] = hc->total_bytes;
+    if (hc->err & kErrPlanes) {
+      cleanup();
+      return kSlabRetryU32;
+    }
     worst = (uint64_t)err_rank(map_err(hc->err)) > worst ? (uint64_t)err_rank(map_err(hc->err)) : worst;
     max_s = hc->max_s > max_s ? hc->max_s : max_s;
   }
@@ -672,6 +742,17 @@ int lopc_compress_slabs_local(const void* in, int ndims, const uint64_t* dims, i
   *out_bytes = total;
   cleanup();
   return LOPC_OK;
+}
+
+int lopc_compress_slabs_local(const void* in, int ndims, const uint64_t* dims, int dtype, double eps, int nslabs,
+                              const uint64_t* bounds, void* out, size_t* out_bytes) {
+  const size_t cap = out_bytes ? *out_bytes : 0;
+  int rc = compress_slabs_local_impl(in, ndims, dims, dtype, eps, nslabs, bounds, out, out_bytes, g_engine == 0);
+  if (rc == kSlabRetryU32) {
+    *out_bytes = cap;
+    rc = compress_slabs_local_impl(in, ndims, dims, dtype, eps, nslabs, bounds, out, out_bytes, false);
+  }
+  return rc;
 }
 
 size_t lopc_decompress_slab_workspace_bytes(uint64_t n_chunks_local) {

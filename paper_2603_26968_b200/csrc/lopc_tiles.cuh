@@ -108,6 +108,7 @@ struct TileArgs {
   uint32_t ntiles[2];
   int max_passes;
   int prof;
+  int q0;  // first pass: 1 (all tiles of tiling 0, unseeded), or 2 (slab rounds: the list of tiling 1 built by k_ghost_inject_tiles)
 };
 
 struct TileWarpSmem {
@@ -448,7 +449,7 @@ __global__ void __launch_bounds__(kTileThreads, LOPC_TILE_CTAS) k_tiles(TileArgs
   uint32_t my_max = 0;
   unsigned long long my_changed = 0;
   const uint64_t t_start = (a.prof && tid == 0 && blockIdx.x == 0) ? gtimer() : 0;
-  int q = 1;
+  int q = a.q0;
   for (; q <= a.max_passes; ++q) {
     const int tiling = (q - 1) & 1;
     const uint32_t n = q == 1 ? a.ntiles[0] : *(volatile uint32_t*)&a.ctr->tl_count[q % 3];
@@ -506,6 +507,67 @@ __global__ void __launch_bounds__(256) k_planes_to_s(const uint32_t* __restrict_
     for (int b = 0; b < kSP; ++b) v |= ((w[b] >> lane) & 1u) << b;
     if (x < d2) __stcs(&s[row * d2 + x], v);
   }
+}
+
+// Slab mode on the tile engine: ghost points (box points
+// owned by a neighbour rank) have no incoming arcs here, so no tile ever
+// changes them; their subbins arrive from the owner after each round.  A
+// ghost whose value rose gets its plane bits rewritten (one thread per
+// point, each bit owned by one thread: per-bit atomics, no lost updates
+// between the points of one segment) and marks the tiles of tiling 1 that
+// hold its star neighbours, with the level hint old + 1 (its level sets
+// changed from level old + 1 up), for the seeded first pass (q0 = 2) of the
+// next k_tiles launch.  ctr->ghost_changed counts the raised ghosts (the
+// round's termination term, summed over ranks).
+template <int NDIM>
+__global__ void __launch_bounds__(256) k_ghost_inject_tiles(TileArgs a, const uint32_t* __restrict__ recv, int64_t g0,
+                                                            int64_t count) {
+  using G = TG<NDIM>;
+  const int lane = threadIdx.x & 31;
+  const int64_t d0 = a.d0, d1 = a.d1, d2 = a.d2, plane = d1 * d2;
+  unsigned changed = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t p = g0 + i;
+    const int64_t z = p / plane, r2 = p - z * plane, y = r2 / d2, x = r2 - y * d2;
+    uint32_t* w = a.sp + ((size_t)(z * d1 + y) * (size_t)a.nseg + (size_t)(x >> 5)) * kSP;
+    const uint32_t bit = 1u << (x & 31);
+    uint32_t old = 0;
+#pragma unroll
+    for (int b = 0; b < kSP; ++b) old |= ((__ldcg(w + b) & bit) ? 1u : 0u) << b;
+    const uint32_t v = __ldg(&recv[i]);
+    if (v <= old) continue;
+    ++changed;
+    if (v > (uint32_t)kMaxPlaneLevel) {  // does not fit 8 planes: the caller re-runs on the u32 engine
+      atomicOr(&a.ctr->err, kErrPlanes);
+      continue;
+    }
+#pragma unroll
+    for (int b = 0; b < kSP; ++b) {
+      const uint32_t nb = (v >> b) & 1u, ob = (old >> b) & 1u;
+      if (nb && !ob) atomicOr(w + b, bit);
+      if (!nb && ob) atomicAnd(w + b, ~bit);
+    }
+    // tiles of tiling 1 holding a star neighbour (the 3x3x3 box around p, clipped)
+    const uint32_t mw = 256u - (old + 1u);
+    const int64_t sz = G::SZ, sy = G::SY;
+    const uint32_t ntz = a.nt[1][0], nty = a.nt[1][1], ntx = a.nt[1][2];
+    const int64_t tz0 = (z - (NDIM == 3 ? 1 : 0) + sz) / G::TZ, tz1 = (z + (NDIM == 3 ? 1 : 0) + sz) / G::TZ;
+    const int64_t ty0 = (y - 1 + sy) / G::TY, ty1 = (y + 1 + sy) / G::TY;
+    const int64_t tx0 = (x > 0 ? x - 1 : 0) >> 5, tx1 = (x + 1 < d2 ? x + 1 : x) >> 5;
+    for (int64_t tz = tz0; tz <= tz1; ++tz)
+      for (int64_t ty = ty0; ty <= ty1; ++ty)
+        for (int64_t tx = tx0; tx <= tx1; ++tx) {
+          if (tz < 0 || tz >= ntz || ty < 0 || ty >= nty) continue;
+          const uint32_t id = (uint32_t)((tz * nty + ty) * ntx + tx);
+          if (atomicMax(&a.act[1][id], mw) == 0u) {
+            const uint32_t slot = atomicAdd(&a.ctr->tl_count[2], 1u);
+            a.list[1][slot] = id;
+          }
+        }
+  }
+  (void)d0;
+  changed = __reduce_add_sync(0xffffffffu, changed);
+  if (lane == 0 && changed) atomicAdd(&a.ctr->ghost_changed, (unsigned long long)changed);
 }
 
 }  // namespace lopc

@@ -35,8 +35,17 @@ CASES = [((24, 40, 50), "f32", "smooth", 2), ((24, 40, 50), "f64", "ties", 3), (
          ((400, 300), "f32", "smooth", 3), ((600, 130), "f64", "plateau", 2), ((40, 64, 64), "f32", "grid16", 4)]
 
 
+@pytest.fixture
+def engine(gpu, request):
+    """Slab mode on the tile engine (0, the default) or the u32 engine (2)."""
+    gpu.set_repair_engine(request.param)
+    yield request.param
+    gpu.set_repair_engine(0)
+
+
+@pytest.mark.parametrize("engine", [0, 2], indirect=True)
 @pytest.mark.parametrize("shape,dt,kind,world", CASES)
-def test_slabs_local_equal_oracle(ref, gpu, shape, dt, kind, world):
+def test_slabs_local_equal_oracle(ref, gpu, engine, shape, dt, kind, world):
     x = random_field(shape, dt, kind, 11)
     eps = eps_noa(x, 1e-2)
     st_ref = ref.compress(x, eps)
@@ -48,9 +57,12 @@ def test_slabs_local_equal_oracle(ref, gpu, shape, dt, kind, world):
     assert st == st_ref
 
 
-def test_chains_cross_slab_boundaries(ref, gpu):
+@pytest.mark.parametrize("engine", [0, 2], indirect=True)
+def test_chains_cross_slab_boundaries(ref, gpu, engine):
     """Decreasing ramps along the linear order: subbins n-1..0 must flow
-    across every slab boundary (several exchange rounds)."""
+    across every slab boundary (several exchange rounds).  Subbins reach
+    23999: on the tile engine the call overflows the 8 subbin planes and
+    every slab re-runs on the u32 engine (same bytes)."""
     x = (1.0 - 1e-7 * np.arange(30 * 20 * 40)).astype(np.float32).reshape(30, 20, 40)
     for world in (2, 3, 5):
         import torch
@@ -62,6 +74,25 @@ def test_chains_cross_slab_boundaries(ref, gpu):
     y = (1.0 - 1e-6 * np.arange(500 * 33)).astype(np.float32).reshape(500, 33)
     bounds = gpu.slab_partition(y.shape, torch.float32, 4)
     assert gpu.compress_slabs_local(_t(y), 1.0, bounds).cpu().numpy().tobytes() == ref.compress(y, 1.0)
+
+
+@pytest.mark.parametrize("engine", [0, 2], indirect=True)
+def test_short_chains_cross_slab_boundaries(ref, gpu, engine):
+    """Repeated decreasing ramps of 200 points (subbins 199..0: they fit the
+    tile engine's planes) cut by every slab boundary: ghosts raised over
+    several rounds, injected into the planes and re-swept from the marked
+    tiles, must give the oracle's bytes."""
+    import torch
+
+    x = (1.0 - 1e-7 * (np.arange(24 * 30 * 40) % 200)).astype(np.float32).reshape(24, 30, 40)
+    y = (1.0 - 1e-6 * (np.arange(300 * 70) % 230)).astype(np.float32).reshape(300, 70)
+    for z in (x, y):
+        st_ref = ref.compress(z, 1.0)
+        for world in (2, 3, 5):
+            bounds = gpu.slab_partition(z.shape, torch.float32, world)
+            st = gpu.compress_slabs_local(_t(z), 1.0, bounds).cpu().numpy().tobytes()
+            assert st == st_ref, (z.shape, world)
+            assert gpu.last_stats()["max_subbin"] < 255
 
 
 @pytest.mark.parametrize("name,world", [("cfg2s", 3), ("cfg4s", 2), ("cfg2", 4)])
