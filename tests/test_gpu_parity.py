@@ -248,6 +248,33 @@ def test_corrupt_streams(ref, gpu):
         assert (r_ref == 0) == (r_gpu == 0), (pos, r_ref, r_gpu)
 
 
+@pytest.mark.parametrize("shape,dt,kind", [((12, 40, 64), "f32", "noise"), ((10, 30, 70), "f64", "smooth"),
+                                           ((90, 200), "f32", "ties")])
+def test_corrupt_streams_fuzz(ref, gpu, shape, dt, kind):
+    """1-4 random bytes of the table or the payloads flipped (multi-chunk
+    streams, both dtypes): the decoder, which reads the payloads in place,
+    must neither fault nor accept what the oracle rejects (P:218 decoder;
+    DESIGN.md §5)."""
+    import torch
+
+    x = random_field(shape, dt, kind, 4)
+    st = ref.compress(x, eps_noa(x, 1e-2))
+    rng = np.random.default_rng(1)
+    for _ in range(60):
+        b = bytearray(st)
+        for _ in range(int(rng.integers(1, 5))):
+            pos = int(rng.integers(64, len(b)))
+            b[pos] ^= int(rng.integers(1, 256))
+        r_ref = ref.decompress_rc(bytes(b), x.shape, x.dtype)
+        try:
+            gpu.decompress(torch.from_numpy(np.frombuffer(bytes(b), np.uint8).copy()).cuda())
+            r_gpu = 0
+        except gpu.LopcError as e:
+            r_gpu = e.code
+        assert r_gpu in (0, -4) and (r_ref == 0) == (r_gpu == 0), (r_ref, r_gpu)
+    torch.cuda.synchronize()
+
+
 def test_determinism_repeat(ref, gpu):
     x = CONFIGS["cfg2"].generate((16, 64, 96))
     eps = eps_noa(x, 1e-3)

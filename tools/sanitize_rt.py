@@ -32,3 +32,37 @@ for engine in (0, 2):
         print(f"engine {engine} {name} {x.shape}: device {'ok' if ok_dev else 'MISMATCH'}, "
               f"host {'ok' if ok_host else 'MISMATCH'}", flush=True)
 lopc.set_repair_engine(0)
+
+# slab mode (3 slabs of a cfg2 crop, halo rounds through device copies) on both engines
+for engine in (0, 2):
+    lopc.set_repair_engine(engine)
+    x = CONFIGS["cfg2"].generate((24, 100, 100))
+    eps = eps_noa(x, CONFIGS["cfg2"].rel)
+    bounds = lopc.slab_partition(x.shape, torch.float32, 3)
+    st = lopc.compress_slabs_local(torch.from_numpy(x).cuda(), eps, bounds)
+    torch.cuda.synchronize()
+    print(f"slab engine {engine}: {'ok' if st.cpu().numpy().tobytes() == oracle.compress(x, eps) else 'MISMATCH'}",
+          flush=True)
+lopc.set_repair_engine(0)
+
+# corrupt streams: the decoder reads payloads in place (global memory), every
+# read bounded by the payload length -- under memcheck no access may leave
+# the stream's allocation, whatever the corruption (run with
+# PYTORCH_NO_CUDA_MEMORY_CACHING=1 so each tensor is its own allocation)
+rng = np.random.default_rng(7)
+for name, small, dt in (("cfg2", (8, 100, 100), np.float32), ("cfg4", (90, 360), np.float64)):
+    x = CONFIGS[name].generate(small).astype(dt)
+    ref = oracle.compress(x, eps_noa(x, CONFIGS[name].rel))
+    n_ok = n_err = 0
+    for _ in range(40):
+        b = bytearray(ref)
+        for _ in range(int(rng.integers(1, 5))):
+            pos = int(rng.integers(64, len(b)))
+            b[pos] ^= int(rng.integers(1, 256))
+        try:
+            lopc.decompress(torch.from_numpy(np.frombuffer(bytes(b), np.uint8).copy()).cuda())
+            torch.cuda.synchronize()
+            n_ok += 1
+        except lopc.LopcError:
+            n_err += 1
+    print(f"corrupt {name} {dt.__name__}: {n_ok} decoded, {n_err} rejected", flush=True)
