@@ -444,6 +444,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--slab", action="store_true", help="use the slab mode even at N=1 (tests the N>1 path)")
+    ap.add_argument("--engine", type=int, default=0, choices=[0, 1, 2],
+                    help="repair engine (diagnostic; 0 = tile engine, the default; see lopc.set_repair_engine); "
+                         "the per-kernel alg bytes of 'sweep' assume engine 0")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -465,6 +468,8 @@ def main():
 
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     lopc.load()
+    if args.engine:
+        lopc.set_repair_engine(args.engine)
     big = args.config == "cfg5"
     if big:  # one rank's slab of cfg5, generated on the device (8.6 GB f64)
         from synth import turbulence as turb
@@ -645,7 +650,8 @@ def main():
                    "dims": list(x.shape), "eps": eps,
                    "input_sha256": sha256(x_np) if x_np is not None else "generated on the device (synth/turbulence.py)",
                    "l2": "flushed (512 MB write) between steps" if not big else "inputs (8.6 GB) larger than L2",
-                   "parallelism": f"replicas x{world}" if world > 1 else "single GPU"},
+                   "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
+                   **({"repair_engine": args.engine} if args.engine else {})},
         "compress_GBps": raw * world * K / (cm / 1e3) / 1e9,
         "step_ms": {"compress": [round(v, 4) for v in comp_ms], "decompress": [round(v, 4) for v in dec_ms]},
         "decompress_GBps": raw * world * K / (dm / 1e3) / 1e9,
