@@ -394,7 +394,10 @@ def run_slabs(args, rank, world, local):
         med = {kk: statistics.median(v) for kk, v in kern.items()}
         n_loc = e1 - e0
         F = 2 if len(shape) == 3 else 1
-        alg = {"quant_flags": n_loc * (k + F), "sweep": n_loc * (F + 4), "encode": n_loc * (k + 4) + sizes[0],
+        # slab mode: tile pass 1 (F + 1 B/point) + the planes widened to u32
+        # after the repair (1 + 4; later tile passes not counted: a lower
+        # bound); the encoder reads x and the u32 subbins
+        alg = {"quant_flags": n_loc * (k + F), "sweep": n_loc * (F + 6), "encode": n_loc * (k + 4) + sizes[0],
                "place": 2 * sizes[0], "decode_scan": 16 * (-(-n_loc // W)), "decode": sizes[0] + n_loc * k}
         dom = max(med, key=lambda kk: med[kk])
         achieved = alg[dom] / (med[dom] / 1e3) / 1e9 if med[dom] > 0 else 0.0
@@ -604,7 +607,10 @@ def main():
         # planes (F + 1 B/point); every later tile visit (1024 points) reads
         # flags + planes and writes planes (F + 2 B/point)
         "sweep": n * (F + 1) + max(0, statistics.median(tiles) - rep["pass_items"][0]) * 1024 * (F + 2),
-        "encode": n * (k + 4) + nbytes_stream,                             # read x + s, write payloads
+        # planes mode (tile engine): the bin CTAs read x, the subbin CTAs the
+        # subbin planes (1 B/point) and the flags' escape words (1/8 B/point);
+        # both write their payloads
+        "encode": n * (k + 1) + n // 8 + nbytes_stream,
         "place": 2 * nbytes_stream,                                        # staged payloads -> stream
         "decode_scan": 16 * ((n * k + 16383) // 16384),                   # size table in, offsets out
         "decode": nbytes_stream + n * k,                                   # read stream, write x^
