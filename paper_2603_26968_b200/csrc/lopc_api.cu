@@ -99,7 +99,7 @@ int g_force_i64 = 0;  // lopc_set_index64: test switch for the int64 index build
 bool use_i32(const Shape& sh) { return !g_force_i64 && sh.n < (1ull << 31) - (1ull << 24); }
 
 struct CLayout {
-  size_t ctr, bitmap, state, act0, act1, zero_end, plist, flags, s, sp, list0, list1, stage, sizes, off, stage_in,
+  size_t ctr, bitmap, state, act0, act1, cesc, zero_end, plist, flags, s, sp, list0, list1, stage, sizes, off, stage_in,
       stage_out, total;
   uint64_t bmw, nseg;
   int ntz, nty, ntx;
@@ -144,6 +144,8 @@ CLayout compress_layout(const Shape& s, bool host_in, bool host_out) {
   o += al(4 * L.tn[0]);
   L.act1 = o;
   o += al(4 * L.tn[1]);
+  L.cesc = o;  // one bit per chunk: it holds an escape (k_quant_flags -> the subbin encoder)
+  o += al(4 * ((s.C + 31) / 32));
   L.zero_end = o;
   L.plist = o;
   o += al(2 * (use_i32(s) ? 4 : 8) * s.n);  // worklist entries: the index width the kernels will use
@@ -364,6 +366,8 @@ RepairArgs make_repair_args(const Shape& sh, const void* x, double eps, uint8_t*
   ra.skip_dense = 0;
   ra.prof = g_timing >= 2;
   ra.engine = 0;
+  ra.cesc = reinterpret_cast<uint32_t*>(ws + L.cesc);
+  ra.chunk_shift = sh.k == 4 ? 12 : 11;  // log2 of the elements per 16 KiB chunk
   return ra;
 }
 
@@ -740,11 +744,12 @@ int compress_impl(const void* in, int ndims, const uint64_t* dims, int dtype, do
   // repair fills the SMs; with subbin planes the bin CTAs also run a4, which
   // needs the repaired subbins.)
   if ((rc = run_repair(sh, x, eps, ws, L, st, tm, engine, false))) return rc;  // marks 3, 4
-  if (engine == kEngTiles) {  // the encoder reads the subbin planes and the flags' escape words
+  if (engine == kEngTiles) {  // the encoder reads the subbin planes and, in chunks with escapes, the flags' escape words
     ea.sp = reinterpret_cast<const uint32_t*>(ws + L.sp);
     ea.flags = reinterpret_cast<const uint32_t*>(ws + L.flags);
     ea.nseg = (int64_t)L.nseg;
     ea.sw = sh.ndims == 3 ? Geo<3>::SW : Geo<2>::SW;
+    ea.cesc = reinterpret_cast<const uint32_t*>(ws + L.cesc);
   }
   // The two roles are independent (both read only x / the repaired
   // subbins): the subbin grid runs on the side stream beside the bin grid

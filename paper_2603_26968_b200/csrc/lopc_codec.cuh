@@ -849,6 +849,7 @@ __device__ __forceinline__ void bit_inverse_planes(const uint8_t* pb, uint8_t* w
 // k_encode
 // ---------------------------------------------------------------------------
 struct EncodeArgs {
+  const uint32_t* cesc;  // planes mode: bit c set when chunk c holds an escape (from k_quant_flags)
   const void* x;
   const uint32_t* s;
   uint8_t* stage;    // C x 32 KiB staging slots (workspace)
@@ -1104,7 +1105,10 @@ __device__ __forceinline__ void encode_chunk_role(const EncodeArgs& a, const uin
     const uint32_t dr = xg / d2;
     const uint64_t i0 = e0 + 32ull * g;
     uint32_t pl[NPL], esc;
-    gather_group<NPL>(a, r0 + dr, xg - dr * d2, i0 < a.n ? a.n - i0 : 0, b0, SUBS && b0 == 0, pl, esc);
+    // (the escape words only in chunks that hold an escape: k_quant_flags
+    // marks them; a 32-byte sector per segment otherwise)
+    const bool esc_chunk = a.cesc && ((a.cesc[c >> 5] >> (c & 31)) & 1u);
+    gather_group<NPL>(a, r0 + dr, xg - dr * d2, i0 < a.n ? a.n - i0 : 0, b0, SUBS && b0 == 0 && esc_chunk, pl, esc);
     uint32_t nzp = 0;
 #pragma unroll
     for (int b = 0; b < NPL; ++b) {

@@ -201,6 +201,8 @@ struct RepairArgs {
   int skip_dense;          // k_sweep: start with the sparse passes (slab rounds >= 2)
   int prof;                // diagnostic: k_sweep pass times (ns) into ctr->phase[14..15]
   int engine;              // 0: dense tile pass + worklist tail; 1: the paper's point worklist from pass 1 (f2)
+  uint32_t* cesc;          // k_quant_flags: bit c set when chunk c holds an escape (box chunks in slab mode: unused)
+  int chunk_shift;         // log2 of the elements per chunk
 };
 
 __device__ __forceinline__ uint64_t gtimer() {
@@ -557,6 +559,13 @@ __global__ void __launch_bounds__(kRepairThreads, sizeof(T) == 4 ? LOPC_QF_CTAS 
     wv[G::SW - 2] = __ballot_sync(0xffffffffu, lok == kHigh && gz < d0 && gy < d1 && x0 + lane < d2);
     if (lane == 0 && gz < d0 && gy < d1) {
       const Idx rb = (gz * d1 + gy) * d2 + x0;
+      if (wv[G::SW - 2]) {  // the chunk(s) of this segment's escapes (rare): the subbin encoder reads their escape words
+        const uint32_t e = wv[G::SW - 2];
+        const uint64_t c0 = (uint64_t)(rb + (Idx)(__ffs(e) - 1)) >> a.chunk_shift;
+        const uint64_t c1 = (uint64_t)(rb + (Idx)(31 - __clz(e))) >> a.chunk_shift;
+        atomicOr(&a.cesc[c0 >> 5], 1u << (c0 & 31));
+        if (c1 != c0) atomicOr(&a.cesc[c1 >> 5], 1u << (c1 & 31));
+      }
       if (rb < (Idx)a.own_lo || rb + 32 > (Idx)a.own_hi) {
         // slab mode: points outside the owned range get no incoming arcs
         const Idx lo_rel = (Idx)a.own_lo - rb, hi_rel = (Idx)a.own_hi - rb;
