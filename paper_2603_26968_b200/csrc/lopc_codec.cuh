@@ -237,7 +237,18 @@ __device__ __forceinline__ uint32_t level_up_warp(const uint8_t* bi, uint32_t si
   return kcount;
 }
 
-__device__ __forceinline__ void pf_l1_bytes(const void* p) { asm volatile("prefetch.global.L1 [%0];" ::"l"(p)); }
+#ifndef LOPC_DEC_PF
+#define LOPC_DEC_PF 1  // k_decode1: the next chunk's payload prefetched into 0 nothing, 1 L1, 2 L2
+#endif
+__device__ __forceinline__ void pf_l1_bytes(const void* p) {
+#if LOPC_DEC_PF == 1
+  asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+#elif LOPC_DEC_PF == 2
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+#else
+  (void)p;
+#endif
+}
 
 // Byte i of a decoder input: shared memory, or (GIN) the payload in global
 // memory read through L1 (the caller bounds i by the payload length).
