@@ -860,7 +860,8 @@ __device__ __forceinline__ void bit_inverse_planes(const uint8_t* pb, uint8_t* w
 // k_encode
 // ---------------------------------------------------------------------------
 struct EncodeArgs {
-  const uint32_t* cesc;  // planes mode: bit c set when chunk c holds an escape (from k_quant_flags)
+  const uint32_t* cesc;  // planes mode: bit c set when chunk c holds an escape (from k_quant_flags); null = read every escape word
+  uint64_t sp_off;       // planes mode: plane-grid index of element 0 (slab mode: the owned range's offset in the box)
   const void* x;
   const uint32_t* s;
   uint8_t* stage;    // C x 32 KiB staging slots (workspace)
@@ -1099,8 +1100,8 @@ __device__ __forceinline__ void encode_chunk_role(const EncodeArgs& a, const uin
     sm.misc[1] = 0;  // OR over the chunk of the plane-nonzero masks
     sm.misc[2] = 0;  // any escape in the chunk
     if (a.sp) {      // (row, x) of the chunk's first element: one 64-bit division per CTA
-      sm.row0 = e0 / a.d2;
-      sm.x0 = (uint32_t)(e0 - sm.row0 * a.d2);
+      sm.row0 = (e0 + a.sp_off) / a.d2;
+      sm.x0 = (uint32_t)(e0 + a.sp_off - sm.row0 * a.d2);
     }
   }
   __syncthreads();
@@ -1366,7 +1367,7 @@ __device__ __forceinline__ void encode_chunk_role(const EncodeArgs& a, const uin
       if ((uint32_t)i < cnt) {
         I b;
         if (quantize_fast<T>(X[i], a.inv32, a.eps, a.inv, b))
-          w = SUBS ? (U)(a.sp ? subbin_at(a, e0 + (uint64_t)i) : S[i]) : (U)b;
+          w = SUBS ? (U)(a.sp ? subbin_at(a, a.sp_off + e0 + (uint64_t)i) : S[i]) : (U)b;
         else
           w = SUBS ? (U)as_bits(X[i]) : VT<T>::kSentinel;
       }

@@ -67,6 +67,9 @@ struct Geo<2> {
 #ifndef LOPC_SWEEP_CTAS
 #define LOPC_SWEEP_CTAS 3  // k_sweep CTAs per SM (register budget 85; 4 and 5 measured slower)
 #endif
+#ifndef LOPC_QF_CESC_LATE
+#define LOPC_QF_CESC_LATE 1  // k_quant_flags marks the chunks with escapes after its row loop (not in the store path)
+#endif
 #ifndef LOPC_QF_CTAS
 #define LOPC_QF_CTAS 4  // k_quant_flags CTAs (of 512) per SM for f32 (32 registers, no spills: 0.180 -> 0.172 ms on cfg2); f64 keeps 3
 #endif
@@ -518,7 +521,14 @@ __global__ void __launch_bounds__(kRepairThreads, sizeof(T) == 4 ? LOPC_QF_CTAS 
 
   // a1 + a2 (Alg. 1 loop 2): warp w, step k handles tile row (w + 16k): lane = x.
   // Flags leave as one ballot per slot (bit plane); lane 0 stores the segment.
-#pragma unroll
+#if LOPC_QF_CESC_LATE
+  uint32_t escrows = 0;  // bit k: row step k stored a segment with escapes (marked after the loop)
+#endif
+#ifndef LOPC_QF_UNROLL
+#define LOPC_QF_UNROLL 1  // the row loop rolled: 0.856 -> 0.832 ms on cfg3 (unroll 2: 0.842)
+#endif
+  constexpr int kQfUnroll = LOPC_QF_UNROLL;
+#pragma unroll kQfUnroll
   for (int k = 0; k < PPT; ++k) {
     const int row = warp + k * (kRepairThreads / 32);
     const int lz = row / G::TY, ly = row % G::TY;
@@ -557,8 +567,12 @@ __global__ void __launch_bounds__(kRepairThreads, sizeof(T) == 4 ? LOPC_QF_CTAS 
     // the extra scattered 4-byte stores cost k_quant_flags 9 % on cfg3, more
     // than the encoder's sector reads of this word save.)
     wv[G::SW - 2] = __ballot_sync(0xffffffffu, lok == kHigh && gz < d0 && gy < d1 && x0 + lane < d2);
+#if LOPC_QF_CESC_LATE
+    escrows |= (uint32_t)(wv[G::SW - 2] != 0u) << k;
+#endif
     if (lane == 0 && gz < d0 && gy < d1) {
       const Idx rb = (gz * d1 + gy) * d2 + x0;
+#if !LOPC_QF_CESC_LATE
       if (wv[G::SW - 2]) {  // the chunk(s) of this segment's escapes (rare): the subbin encoder reads their escape words
         const uint32_t e = wv[G::SW - 2];
         const uint64_t c0 = (uint64_t)(rb + (Idx)(__ffs(e) - 1)) >> a.chunk_shift;
@@ -566,6 +580,7 @@ __global__ void __launch_bounds__(kRepairThreads, sizeof(T) == 4 ? LOPC_QF_CTAS 
         atomicOr(&a.cesc[c0 >> 5], 1u << (c0 & 31));
         if (c1 != c0) atomicOr(&a.cesc[c1 >> 5], 1u << (c1 & 31));
       }
+#endif
       if (rb < (Idx)a.own_lo || rb + 32 > (Idx)a.own_hi) {
         // slab mode: points outside the owned range get no incoming arcs
         const Idx lo_rel = (Idx)a.own_lo - rb, hi_rel = (Idx)a.own_hi - rb;
@@ -580,6 +595,20 @@ __global__ void __launch_bounds__(kRepairThreads, sizeof(T) == 4 ? LOPC_QF_CTAS 
       for (int q = 0; q < G::SW / 4; ++q) dst[q] = make_uint4(wv[4 * q], wv[4 * q + 1], wv[4 * q + 2], wv[4 * q + 3]);
     }
   }
+#if LOPC_QF_CESC_LATE
+  if (lane == 0 && escrows) {  // rare: the chunks of the row segments with escapes (first and last point: a superset)
+    for (int k = 0; k < PPT; ++k) {
+      if (!((escrows >> k) & 1u)) continue;
+      const int row = warp + k * (kRepairThreads / 32);
+      const Idx gz = z0 + row / G::TY, gy = y0 + row % G::TY;
+      const Idx rb = (gz * d1 + gy) * d2 + x0;
+      const Idx re = rb + (x0 + 32 <= d2 ? 31 : d2 - 1 - x0);
+      const uint64_t c0 = (uint64_t)rb >> a.chunk_shift, c1 = (uint64_t)re >> a.chunk_shift;
+      atomicOr(&a.cesc[c0 >> 5], 1u << (c0 & 31));
+      if (c1 != c0) atomicOr(&a.cesc[c1 >> 5], 1u << (c1 & 31));
+    }
+  }
+#endif
 }
 
 // ---------------------------------------------------------------------------

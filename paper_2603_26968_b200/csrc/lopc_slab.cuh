@@ -137,11 +137,11 @@ struct Slab {
   uint8_t* recv_lo() const { return ws + lay.recv_lo; }
   uint8_t* recv_hi() const { return ws + lay.recv_hi; }
 
-  // the repair of round 1 (after k_quant_flags); with tiles the planes are
-  // widened to u32 after every launch (the halo exchange and the encoder
-  // read u32 subbins)
+  // the repair of round 1 (after k_quant_flags); with tiles the subbins stay
+  // in the planes (the encoder reads them; the halo exchange widens only
+  // the points it sends, widen_send)
   int repair1() {
-    if (tiles) return launch_tiles(geo.box, ra, ws, lay.L, st, true);
+    if (tiles) return launch_tiles(geo.box, ra, ws, lay.L, st, false);
     ra.skip_dense = 0;
     return launch_sweep(geo.box, ra, lay.L, st);
   }
@@ -191,8 +191,22 @@ struct Slab {
     CK(cudaGetLastError());
     return LOPC_OK;
   }
+  // tiles: the u32 subbins of the boundary points this slab sends
+  int widen_send() {
+    if (!tiles) return LOPC_OK;
+    const uint32_t* sp = reinterpret_cast<const uint32_t*>(ws + lay.L.sp);
+    auto wr = [&](uint64_t start, uint64_t cnt) {
+      if (!cnt) return;
+      const unsigned gb = (unsigned)((cnt + 255) / 256 < 1184 ? (cnt + 255) / 256 : 1184);
+      k_planes_range<<<gb, 256, 0, st>>>(sp, s(), (int64_t)geo.box.d2, (int64_t)lay.L.nseg, (int64_t)start, (int64_t)cnt);
+    };
+    wr(own_lo(), geo.send_lo);
+    wr(own_hi() - geo.send_hi, geo.send_hi);
+    CK(cudaGetLastError());
+    return LOPC_OK;
+  }
   int sweep_sparse() {
-    if (tiles) return launch_tiles(geo.box, ra, ws, lay.L, st, true, 2);
+    if (tiles) return launch_tiles(geo.box, ra, ws, lay.L, st, false, 2);
     ra.skip_dense = 1;
     return launch_sweep(geo.box, ra, lay.L, st);
   }
@@ -202,6 +216,14 @@ struct Slab {
     EncodeArgs ea{};
     ea.x = x_own;
     ea.s = s() + own_lo();
+    if (tiles) {  // planes mode: the box's planes and flags, offset by the owned range
+      ea.sp = reinterpret_cast<const uint32_t*>(ws + lay.L.sp);
+      ea.flags = reinterpret_cast<const uint32_t*>(ws + lay.L.flags);
+      ea.nseg = (int64_t)lay.L.nseg;
+      ea.sw = geo.box.ndims == 3 ? Geo<3>::SW : Geo<2>::SW;
+      ea.sp_off = own_lo();
+      ea.cesc = nullptr;  // its chunk bits are per box chunk: read every escape word
+    }
     ea.stage = ws + lay.L.stage;
     ea.sizes = reinterpret_cast<uint32_t*>(ws + lay.L.sizes);
     ea.ctr = dctr();
@@ -502,6 +524,7 @@ int compress_slab_impl(lopc_comm* comm, const void* in_slab, int ndims, const ui
   uint64_t rounds = 1;
   bool broke_on_failure = false;
   while (world > 1) {
+    if (!lrc) lrc = sl.widen_send();
     if ((rc = halo(reinterpret_cast<uint8_t*>(sl.s()), 4, ncclUint32))) return rc;
     if (!lrc) lrc = sl.inject();
     if (!lrc && fault_injected(rank, (int)rounds)) lrc = LOPC_E_INTERNAL;
@@ -572,9 +595,9 @@ int compress_slab_impl(lopc_comm* comm, const void* in_slab, int ndims, const ui
   g_stats.sub_bytes = hc->sub_bytes;
   g_stats.total_bytes = off;
   g_stats.inner_iters = rounds;  // slab mode: repair rounds (halo exchanges + 1)
-  // quant_flags + repair (+ widen), per further round: up to 2 injections +
-  // repair (+ widen); 2 encoder grids, scan, place
-  g_stats.launches = (uint32_t)((tiles ? 3 : 2) + (tiles ? 4 : 3) * (rounds - 1) + 2 + 2);
+  // quant_flags + repair, per further round: (tiles: 2 boundary widens +) up
+  // to 2 injections + repair; 2 encoder grids, scan, place
+  g_stats.launches = (uint32_t)(2 + (tiles ? 5 : 3) * (rounds - 1) + 2 + 2);
   const uint64_t need = 8 * G.C_local + mine[0];
   if (worst == (uint64_t)-kSlabRetryU32) return kSlabRetryU32;
   if (worst) {
@@ -668,6 +691,8 @@ int compress_slabs_local_impl(const void* in, int ndims, const uint64_t* dims, i
   Counters* hc;
   if ((rc = host_ctr(hc))) { cleanup(); return rc; }
   while (nslabs > 1) {
+    for (auto& a : sl)
+      if ((rc = a.widen_send())) { cleanup(); return rc; }
     if ((rc = exchange(false))) { cleanup(); return rc; }
     for (auto& a : sl)
       if ((rc = a.inject())) { cleanup(); return rc; }

@@ -489,6 +489,20 @@ __global__ void __launch_bounds__(kTileThreads, LOPC_TILE_CTAS) k_tiles(TileArgs
   if (lane == 0 && my_max) atomicMax(&a.ctr->max_s, my_max);
 }
 
+// Subbin planes -> u32 for the linear range [start, start + count) of the
+// plane grid (slab mode: the boundary points a halo exchange sends).
+__global__ void __launch_bounds__(256) k_planes_range(const uint32_t* __restrict__ sp, uint32_t* __restrict__ s,
+                                                      int64_t d2, int64_t nseg, int64_t start, int64_t count) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t p = start + i, row = p / d2, x = p - row * d2;
+    const uint32_t* w = sp + ((size_t)row * (size_t)nseg + (size_t)(x >> 5)) * kSP;
+    uint32_t v = 0;
+#pragma unroll
+    for (int b = 0; b < kSP; ++b) v |= ((__ldg(w + b) >> (x & 31)) & 1u) << b;
+    s[p] = v;
+  }
+}
+
 // Subbin planes -> one u32 per point (the encoder's input, and repair_ex).
 template <int NDIM>
 __global__ void __launch_bounds__(256) k_planes_to_s(const uint32_t* __restrict__ sp, uint32_t* __restrict__ s,
