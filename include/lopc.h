@@ -160,7 +160,9 @@ void lopc_set_timing(int enable);
  * paper's point worklist from the first pass (Alg. 2 over every point, then
  * the points whose inputs rose); 2: round 1's dense tile pass
  * then point-worklist passes (u32 subbins).  All reach the same unique least
- * fixpoint (reading G14), hence the same bytes.  Slab mode uses engine 2.
+ * fixpoint (reading G14), hence the same bytes.  Slab mode repairs with
+ * the tile engine for engine 0 (re-running every rank on engine 2 when a
+ * subbin exceeds 8 planes anywhere) and with engine 2 otherwise.
  * E_ARG for another value. */
 int lopc_set_repair_engine(int engine);
 
@@ -254,7 +256,9 @@ int lopc_compress_noa(const void* in, int ndims, const uint64_t* dims, int dtype
  * the ranges and local checks), after every repair round (the round's
  * allreduce carries a failure count, so a rank that fails locally keeps
  * taking part in the collectives and all ranks stop together) and at exit
- * (an allgather of sizes and codes).  A failing NCCL call itself returns
+ * (an allgather of sizes and codes).  A subbin above 8 planes on any rank
+ * (tile engine) is agreed the same way and every rank re-runs the call on
+ * the u32 engine internally (same bytes).  A failing NCCL call itself returns
  * LOPC_E_NCCL at once; the communicator is then unusable.  A NULL comm means
  * world = 1.  SURVEY §8(e); the exchange is the one of Alg. 2's sweeps
  * across slab boundaries.
