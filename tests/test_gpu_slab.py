@@ -77,6 +77,28 @@ def test_chains_cross_slab_boundaries(ref, gpu, engine):
 
 
 @pytest.mark.parametrize("engine", [0, 2], indirect=True)
+@pytest.mark.parametrize("dt", ["f32", "f64"])
+def test_slab_escapes(ref, gpu, engine, dt):
+    """NaN, +-Inf and out-of-range values (escapes, G8-G11) in several slabs,
+    one beside a slab boundary: the slab encoder (planes mode on the tile
+    engine) must store them raw exactly as the oracle does."""
+    import torch
+
+    x = random_field((24, 40, 50), dt, "smooth", 8)
+    eps = eps_noa(x, 1e-2)
+    big = 3e38 if dt == "f32" else 1e300
+    n = x.size
+    for i, v in zip([0, 7, n // 3, n // 2 - 1, n // 2, 2 * n // 3 + 5, n - 1],
+                    [np.nan, np.inf, -np.inf, big, np.nan, -big, np.inf]):
+        x.ravel()[i] = v
+    tdt = torch.float32 if dt == "f32" else torch.float64
+    for world in (2, 3):
+        bounds = gpu.slab_partition(x.shape, tdt, world)
+        st = gpu.compress_slabs_local(_t(x), eps, bounds).cpu().numpy().tobytes()
+        assert st == ref.compress(x, eps), world
+
+
+@pytest.mark.parametrize("engine", [0, 2], indirect=True)
 def test_short_chains_cross_slab_boundaries(ref, gpu, engine):
     """Repeated decreasing ramps of 200 points (subbins 199..0: they fit the
     tile engine's planes) cut by every slab boundary: ghosts raised over
