@@ -103,7 +103,7 @@ if os.path.exists(lp):
     lines = [ln for ln in open(lp) if ln.startswith('"')]
     lr = list(csv.reader(lines))
     h = lr[0]
-    keep = [h] + [r for r in lr[1:] if "lopc::" in r[h.index("Kernel Name")]]
+    keep = [h] + [r for r in lr[1:] if short(r[h.index("Kernel Name")]).startswith("k_")]
     with open(os.path.join(prof, f"{tag}_launches.csv"), "w", newline="") as f:
         csv.writer(f).writerows(keep)
     tot = {}
