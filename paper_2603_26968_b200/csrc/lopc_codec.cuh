@@ -1118,8 +1118,9 @@ __device__ __forceinline__ void encode_chunk_role(const EncodeArgs& a, const uin
     const uint64_t i0 = e0 + 32ull * g;
     uint32_t pl[NPL], esc;
     // (the escape words only in chunks that hold an escape: k_quant_flags
-    // marks them; a 32-byte sector per segment otherwise)
-    const bool esc_chunk = a.cesc && ((a.cesc[c >> 5] >> (c & 31)) & 1u);
+    // marks them; a 32-byte sector per segment otherwise.  No chunk bits
+    // (slab mode): every chunk reads them)
+    const bool esc_chunk = !a.cesc || ((a.cesc[c >> 5] >> (c & 31)) & 1u);
     gather_group<NPL>(a, r0 + dr, xg - dr * d2, i0 < a.n ? a.n - i0 : 0, b0, SUBS && b0 == 0 && esc_chunk, pl, esc);
     uint32_t nzp = 0;
 #pragma unroll
