@@ -74,7 +74,7 @@ struct Geo<2> {
 #define LOPC_QF_CTAS 4  // k_quant_flags CTAs (of 512) per SM for f32 (32 registers, no spills: 0.180 -> 0.172 ms on cfg2); f64 keeps 3
 #endif
 #ifndef LOPC_SUBS_CTAS
-#define LOPC_SUBS_CTAS 5  // k_encode<T, 2> (subbin stream) CTAs per SM: 48 registers, no spills (1 % faster than 6)
+#define LOPC_SUBS_CTAS 6  // k_encode<T, 2> (subbin stream) CTAs per SM: 40 registers (r2: with the planes-mode subbin role 1.4-1.8 % faster than 5)
 #endif
 #ifndef LOPC_CODEC_CTAS
 #define LOPC_CODEC_CTAS 6  // k_encode / k_decode CTAs per SM (register budget 40; 4 and 5 measured slower)
