@@ -183,12 +183,17 @@ bool is_device_ptr(const void* p) {
   return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
 }
 
+#ifndef LOPC_PIPE_RANGES
+#define LOPC_PIPE_RANGES 8
+#endif
+constexpr int kPipeRanges = LOPC_PIPE_RANGES;  // host-I/O decompress pipeline depth (4 in r1)
+
 struct DevInfo {
   int dev = -1, sms = 0;
   cudaStream_t side = nullptr;           // bin-stream encode runs here, beside the repair
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   cudaStream_t side2 = nullptr;            // host-I/O decompress: D2H of decoded ranges
-  cudaEvent_t ev_in[4] = {}, ev_dec[4] = {}, ev_out = nullptr;
+  cudaEvent_t ev_in[kPipeRanges] = {}, ev_dec[kPipeRanges] = {}, ev_out = nullptr;
   int occ_sweep2 = 0, occ_sweep3 = 0, occ_sweep2w = 0, occ_sweep3w = 0, occ_decode = 0, occ_tiles2 = 0, occ_tiles3 = 0;
   int occ_decode1 = 0;
   bool attrs = false;
@@ -209,7 +214,7 @@ int dev_info(DevInfo*& out) {
     CK(cudaEventCreateWithFlags(&g_dev.ev_fork, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&g_dev.ev_join, cudaEventDisableTiming));
     CK(cudaStreamCreateWithFlags(&g_dev.side2, cudaStreamNonBlocking));
-    for (int i = 0; i < 4; ++i) {
+    for (int i = 0; i < kPipeRanges; ++i) {
       CK(cudaEventCreateWithFlags(&g_dev.ev_in[i], cudaEventDisableTiming));
       CK(cudaEventCreateWithFlags(&g_dev.ev_dec[i], cudaEventDisableTiming));
     }
@@ -1000,8 +1005,8 @@ int lopc_decompress_ex(const void* in, size_t in_bytes, void* out, size_t out_ca
   Timer tm;
   if ((rc = tm.init(st))) return rc;
   g_stats = lopc_stats{};
-  // Host stream -> host values, per-kernel timing off: a pipeline of up to 4
-  // chunk ranges — H2D of range i's payloads (stream st), k_decode of range i
+  // Host stream -> host values, per-kernel timing off: a pipeline of up to
+  // kPipeRanges chunk ranges — H2D of range i's payloads (stream st), k_decode of range i
   // (side stream, after its H2D), D2H of its values (second side stream,
   // after its decode) — so the PCIe copies overlap the decode.  Offsets come
   // from the host copy of the size table (validated as k_chunk_scan would).
@@ -1019,7 +1024,7 @@ int lopc_decompress_ex(const void* in, size_t in_bytes, void* out, size_t out_ca
     CK(cudaEventRecord(di->ev_fork, st));
     CK(cudaStreamWaitEvent(di->side, di->ev_fork, 0));
     CK(cudaStreamWaitEvent(di->side2, di->ev_fork, 0));
-    const int K = C < 4 ? (int)C : 4;
+    const int K = C < (uint32_t)kPipeRanges ? (int)C : kPipeRanges;
     for (int i = 0; i < K; ++i) {
       const uint64_t cb = (uint64_t)C * i / K, ce = (uint64_t)C * (i + 1) / K;
       const uint64_t b0 = hoff[cb], b1 = ce == C ? in_bytes : hoff[ce];

@@ -14,7 +14,8 @@ for so in sorted(glob.glob("variants/liblopc_*.so")):
     try:
         d = json.loads(r.stdout.strip().splitlines()[-1])
         pk = {k: round(v["ms"], 4) for k, v in d["per_kernel"].items()}
-        print(os.path.basename(so), f"value {d['value']:.1f} comp {d['compress_GBps']:.1f} dec {d['decompress_GBps']:.1f}",
+        print(os.path.basename(so), f"value {d['value']:.1f} comp {d['compress_GBps']:.1f} dec {d['decompress_GBps']:.1f}"
+              f" e2e {d['e2e']['value']:.2f}",
               pk, "viol", d["order_violations"], d["bound_violations"], flush=True)
     except Exception as e:  # noqa: BLE001
         print(os.path.basename(so), "FAILED", e, r.stderr[-2000:], flush=True)
