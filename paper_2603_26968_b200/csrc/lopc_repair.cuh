@@ -70,6 +70,9 @@ struct Geo<2> {
 #ifndef LOPC_QF_CESC_LATE
 #define LOPC_QF_CESC_LATE 1  // k_quant_flags marks the chunks with escapes after its row loop (not in the store path)
 #endif
+#ifndef LOPC_QF_CTAS64
+#define LOPC_QF_CTAS64 3  // k_quant_flags CTAs (of 512) per SM for f64 (4: 32 registers, 9.29 -> 9.42 ms on cfg5)
+#endif
 #ifndef LOPC_QF_CTAS
 #define LOPC_QF_CTAS 4  // k_quant_flags CTAs (of 512) per SM for f32 (32 registers, no spills: 0.180 -> 0.172 ms on cfg2); f64 keeps 3
 #endif
@@ -410,7 +413,7 @@ constexpr size_t quant_flags_smem() {
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
 template <typename T, int NDIM, typename Idx, bool TMA>
-__global__ void __launch_bounds__(kRepairThreads, sizeof(T) == 4 ? LOPC_QF_CTAS : 3) k_quant_flags(RepairArgs a, const __grid_constant__ CUtensorMap tmap) {
+__global__ void __launch_bounds__(kRepairThreads, sizeof(T) == 4 ? LOPC_QF_CTAS : LOPC_QF_CTAS64) k_quant_flags(RepairArgs a, const __grid_constant__ CUtensorMap tmap) {
   using G = Geo<NDIM>;
   using I = typename VT<T>::I;
   using U = typename VT<T>::U;
